@@ -1,0 +1,64 @@
+"""One verify step for one session (in order).
+
+Alg-S Listener: verify the draft at every exit, push the
+early-exit results with their score, send the final result flagged final.
+This oracle runs one early exit l_e plus the final exit (the north star's
+configuration; all-exits is its repetition).
+
+The query block is [pending, x_1..x_gamma] at positions ctx..ctx+gamma
+(R15).  After the final acceptance the cache is rolled back to
+ctx + 1 + delta rows: the pending token plus the accepted drafts (R22);
+the emitted correction / bonus token becomes the next step's pending token.
+The early exit shares the final exit's Philox counters (R10) and never
+changes the session (its output is read-only: "all tokens are verified at the
+final exit").
+"""
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import accept as acc
+from .model import KVCache, Model, forward
+
+
+@dataclass
+class Session:
+    session_id: int
+    philox_seed: int
+    cache: KVCache
+    last_round: int = 0
+
+
+@dataclass
+class StepOut:
+    final: acc.Result
+    early: acc.Result
+    final_logits: np.ndarray
+    exit_logits: np.ndarray
+    new_len: int
+
+
+def verify_step(model: Model, sess: Session, round_id: int, pending: int, drafts,
+                probs=None, exit_layer: int = 0) -> StepOut:
+    cfg = model.cfg
+    drafts = [int(x) for x in drafts]
+    gamma = len(drafts)
+    if not (1 <= gamma <= 8):
+        raise ValueError("gamma must be in 1..8")
+    if round_id != sess.last_round + 1:
+        bad = acc.Result(0, [], 0.0, 0.0, acc.E_PROTOCOL, [])
+        return StepOut(bad, bad, None, None, sess.cache.length)
+    ctx = sess.cache.length
+    block = np.array([pending] + drafts, dtype=np.int64)
+    z, ze, _ = forward(model, sess.cache, block, exit_layer)
+    kw = dict(seed=sess.philox_seed, session_id=sess.session_id, round_id=round_id)
+    q = None if probs is None else np.asarray(probs, dtype=np.float64)
+    final = acc.accept(z, drafts, q, **kw)
+    early = acc.accept(ze, drafts, q, **kw) if ze is not None else None
+    if final.status != acc.OK:
+        sess.cache.truncate(ctx)                      # protocol error: KV not advanced
+        return StepOut(final, early, z, ze, ctx)
+    new_len = ctx + 1 + final.accepted
+    sess.cache.truncate(new_len)                      # S14 rollback
+    sess.last_round = round_id
+    return StepOut(final, early, z, ze, new_len)

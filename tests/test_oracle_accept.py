@@ -1,0 +1,184 @@
+"""Pins for oracle/accept.py.
+
+- SPEC.md worked examples (greedy SPEC.md:120-123, residual SPEC.md:139-142,
+  confidence SPEC.md:62-66), translated to survey letters (p = target).
+- Brute force: greedy delta == longest prefix with x_j == argmax row j-1.
+- Leviathan's theorem (adopted): with x_j ~ q_j the emitted
+  token at position 1 is distributed as p_0, and conditional on acceptance of
+  x_1 the token at position 2 is distributed as p_1 (chi-square, alpha=1e-3);
+  per-position acceptance frequency equals E_x~q[min(1, p(x)/q(x))] = sum_v min(p, q).
+- Special cases: q == p accepts everything; p(x_j) = 0 always
+  rejects; q(x_j) = 0 is a protocol error.
+- Exponential race: draws follow normalize(w) (chi-square).
+"""
+import numpy as np
+import pytest
+from scipy import stats
+
+from oracle import accept as acc
+from oracle import philox
+
+
+def _logits_with_argmax(ids, V=12, gap=2.0, seed=0):
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal((len(ids), V))
+    for r, a in enumerate(ids):
+        z[r, a] = z[r].max() + gap
+    return z
+
+
+def test_spec_greedy_examples():
+    z = _logits_with_argmax([5, 7, 9, 2])
+    r = acc.accept_greedy(z, [5, 7, 9])
+    assert r.accepted == 3 and r.tokens == [5, 7, 9, 2]
+    z = _logits_with_argmax([5, 8, 1, 3])
+    r = acc.accept_greedy(z, [5, 7, 9])
+    assert r.accepted == 1 and r.tokens == [5, 8]
+
+
+def test_spec_residual_examples():
+    assert np.allclose(acc.residual_distribution([0.2, 0.5, 0.3], [0.6, 0.3, 0.1]), [0, 0.5, 0.5])
+    assert np.allclose(acc.residual_distribution([0.5, 0.5], [1.0, 0.0]), [0, 1])
+    assert np.allclose(acc.residual_distribution([1.0, 0.0], [0.0, 1.0]), [1, 0])
+    with pytest.raises(ValueError):
+        acc.residual_distribution([0.5, 0.5], [0.5, 0.5])
+
+
+def test_spec_confidence_examples():
+    assert acc.confidence(acc.softmax(np.zeros(4))) == pytest.approx(0.25)
+    assert acc.confidence(acc.softmax(np.array([0.0, -1e4, -1e4]))) == pytest.approx(1.0)
+    assert acc.confidence(acc.softmax(np.array([np.log(2.0), 0.0, 0.0]))) == pytest.approx(0.5)
+
+
+def test_greedy_tie_lowest_index():
+    z = np.zeros((2, 5)); z[0, [1, 3]] = 1.0; z[1, 0] = 1.0
+    assert acc.accept_greedy(z, [3]).tokens == [1]
+    assert acc.accept_greedy(z, [1]).tokens == [1, 0]
+
+
+def test_greedy_brute_force_random():
+    rng = np.random.default_rng(7)
+    for _ in range(300):
+        V, gamma = int(rng.integers(2, 6)), int(rng.integers(1, 9))
+        z = rng.integers(0, 3, size=(gamma + 1, V)).astype(float)      # many ties
+        drafts = rng.integers(0, V, size=gamma)
+        # brute force: enumerate delta as the largest k with all x_j == argmax(row j-1)
+        best = 0
+        for k in range(1, gamma + 1):
+            if all(drafts[j - 1] == min(np.flatnonzero(z[j - 1] == z[j - 1].max())) for j in range(1, k + 1)):
+                best = k
+        r = acc.accept_greedy(z, drafts)
+        assert r.accepted == best
+        assert r.tokens[:best] == list(drafts[:best])
+        assert r.tokens[best] == min(np.flatnonzero(z[best] == z[best].max()))
+        assert len(r.tokens) == best + 1
+
+
+def test_score_is_max_confidence_over_emitted_rows():
+    z = np.array([[3.0, 0, 0], [0, 0.1, 0], [0, 0, 9.0]])
+    r = acc.accept_greedy(z, [0, 1])      # row0 argmax 0 -> accept; row1 argmax 1 -> accept; bonus row2
+    assert r.accepted == 2
+    assert r.score == pytest.approx(max(acc.softmax(z[k]).max() for k in range(3)))
+    r = acc.accept_greedy(z, [1, 1])      # reject at row 0: only row 0 counts
+    assert r.accepted == 0 and r.score == pytest.approx(acc.softmax(z[0]).max())
+    assert r.next_prob == pytest.approx(acc.softmax(z[0])[0])
+
+
+def _rows(rng, n, V, conc=1.0):
+    return rng.dirichlet(np.full(V, conc), size=n)
+
+
+def test_q_equals_p_accepts_all():
+    rng = np.random.default_rng(1)
+    gamma, V = 4, 7
+    p = _rows(rng, gamma + 1, V)
+    z = np.log(p)
+    for rnd in range(1, 200):
+        x = [rng.choice(V, p=p[j]) for j in range(gamma)]
+        r = acc.accept_stochastic(z, x, p[:gamma], seed=4, session_id=1, round_id=rnd)
+        assert r.accepted == gamma and r.tokens[:gamma] == x
+
+
+def test_zero_target_mass_always_rejected():
+    rng = np.random.default_rng(2)
+    V = 5
+    p0 = np.array([0.0, 0.4, 0.3, 0.2, 0.1])
+    with np.errstate(divide="ignore"):
+        z = np.log(np.stack([p0, _rows(rng, 1, V)[0]]))
+    q = np.array([[0.5, 0.2, 0.1, 0.1, 0.1]])
+    seen = set()
+    for rnd in range(1, 300):
+        r = acc.accept_stochastic(z, [0], q, seed=4, session_id=1, round_id=rnd)
+        assert r.accepted == 0 and r.tokens[0] != 0
+        seen.add(r.tokens[0])
+    # replacement follows normalize(max(0, p0 - q)) = [0, .2, .2, .1, 0]/.5: tokens 1..3 only
+    assert seen <= {1, 2, 3} and len(seen) == 3
+
+
+def test_zero_draft_mass_is_protocol_error():
+    z = np.zeros((2, 3))
+    r = acc.accept_stochastic(z, [1], np.array([[0.5, 0.0, 0.5]]), seed=1, session_id=1, round_id=1)
+    assert r.status == acc.E_PROTOCOL
+
+
+def test_leviathan_law_chi_square():
+    """Emitted token law equals the target law (position 1, and position 2 given
+    x_1 accepted), with context-independent target rows."""
+    rng = np.random.default_rng(3)
+    V, gamma, N = 6, 2, 20000
+    p = _rows(rng, gamma + 1, V, conc=2.0)
+    q = _rows(rng, gamma, V, conc=2.0)
+    z = np.log(p)
+    first = np.zeros(V)
+    second = np.zeros(V)
+    acc_first = 0
+    for t in range(N):
+        x = [rng.choice(V, p=q[j]) for j in range(gamma)]
+        r = acc.accept_stochastic(z, x, q, seed=11, session_id=5, round_id=t + 1)
+        first[r.tokens[0]] += 1
+        if r.accepted >= 1:
+            acc_first += 1
+            second[r.tokens[1]] += 1
+    assert stats.chisquare(first, N * p[0]).pvalue > 1e-3
+    n2 = second.sum()
+    assert stats.chisquare(second, n2 * p[1]).pvalue > 1e-3
+    # acceptance rate of x_1: alpha = sum_v min(p0, q1)
+    alpha = np.minimum(p[0], q[0]).sum()
+    assert stats.binomtest(acc_first, N, alpha).pvalue > 1e-3
+
+
+def test_race_law_chi_square():
+    w = np.array([0.0, 3.0, 1.0, 0.5, 0.0, 5.5])
+    N = 40000
+    counts = np.zeros(len(w))
+    for t in range(N):
+        u = philox.uniforms(9, 2, t, 0, philox.PURPOSE_RACE, len(w))
+        v, _ = acc.race(w, u)
+        counts[v] += 1
+    assert counts[0] == 0 and counts[4] == 0
+    nz = w > 0
+    assert stats.chisquare(counts[nz], N * w[nz] / w.sum()).pvalue > 1e-3
+
+
+def test_acceptance_chain_probability():
+    """P(delta >= k | drafts) = prod_{j<=k} min(1, p_{j-1}(x_j)/q_j(x_j)) for fixed drafts."""
+    rng = np.random.default_rng(4)
+    V, gamma, N = 5, 3, 6000
+    p = _rows(rng, gamma + 1, V, conc=3.0)
+    q = _rows(rng, gamma, V, conc=3.0)
+    z = np.log(p)
+    x = [int(np.argmax(q[j])) for j in range(gamma)]
+    ge = np.zeros(gamma + 1)
+    for t in range(N):
+        r = acc.accept_stochastic(z, x, q, seed=12, session_id=3, round_id=t + 1)
+        ge[:r.accepted + 1] += 1
+    for k in range(1, gamma + 1):
+        pk = np.prod([min(1.0, p[j - 1][x[j - 1]] / q[j - 1][x[j - 1]]) for j in range(1, k + 1)])
+        assert stats.binomtest(int(ge[k]), N, pk).pvalue > 1e-3
+
+
+def test_margins_recorded():
+    z = _logits_with_argmax([1, 2, 3], V=6, gap=0.5)
+    r = acc.accept_greedy(z, [1, 2])
+    assert [k for k, _, _ in r.margins] == ["argmax", "argmax", "argmax"]
+    assert r.min_margin == pytest.approx(0.5)

@@ -1,0 +1,101 @@
+"""Pins for oracle/verify.py (one verify step on a session).
+
+- l_e = L: the early-exit result equals the final result exactly (north star).
+- Rollback (R22): new length = ctx + 1 + delta; rows [0, ctx) unchanged;
+  the rolled-back cache equals a full causal recompute of prefix + [pending,
+  x_1..x_delta] (invariant: KV-incremental + rollback == recompute).
+- Protocol errors leave the session unchanged.
+- Multi-round greedy decoding with an oracle-perfect drafter accepts everything.
+"""
+import numpy as np
+
+from oracle import accept as acc
+from oracle import model as om
+from oracle.verify import Session, verify_step
+from workload import tiny
+from workload.drafts import timing_drafts
+
+
+def _session(cfg, m, ctx=20, seed=4, sid=1, prefill=True):
+    cache = om.KVCache(cfg)
+    if prefill:
+        toks = np.random.default_rng(sid).integers(0, cfg.vocab, size=ctx)
+        om.forward(m, cache, toks)
+    else:
+        cache = om.KVCache.synthetic(cfg, 2, ctx)
+    return Session(sid, seed, cache)
+
+
+def test_exit_at_last_layer_equals_final():
+    cfg = tiny()
+    m = om.Model(cfg, 1)
+    for mode in ("greedy", "stochastic"):
+        s = _session(cfg, m)
+        x, q = timing_drafts(3, 1, 4, cfg.vocab)
+        out = verify_step(m, s, 1, 7, x[0], q[0] if mode == "stochastic" else None,
+                          exit_layer=cfg.n_layers)
+        assert out.early.accepted == out.final.accepted
+        assert out.early.tokens == out.final.tokens
+        assert out.early.score == out.final.score
+        assert np.array_equal(out.exit_logits, out.final_logits)
+
+
+def test_rollback_equals_recompute():
+    cfg = tiny()
+    m = om.Model(cfg, 1)
+    s = _session(cfg, m, ctx=15)
+    prefix_k = [k.copy() for k in s.cache.k]
+    # drafts: the target's own greedy continuation for 2 tokens then a wrong token
+    c = s.cache.copy()
+    z, _, _ = om.forward(m, c, [9])
+    a1 = int(np.argmax(z[0]))
+    c = s.cache.copy()
+    z, _, _ = om.forward(m, c, [9, a1])
+    a2 = int(np.argmax(z[1]))
+    bad = (a2 + 1) % cfg.vocab
+    out = verify_step(m, s, 1, 9, [a1, a2, bad, 3], None, exit_layer=1)
+    assert out.final.accepted == 2 and out.final.tokens[:2] == [a1, a2]
+    assert out.new_len == 15 + 1 + 2 and s.cache.length == 18
+    for l in range(cfg.n_layers):
+        assert np.array_equal(s.cache.k[l][:, :15], prefix_k[l])
+    # full recompute of prefix + [pending, a1, a2]
+    toks = np.random.default_rng(1).integers(0, cfg.vocab, size=15)
+    full = om.KVCache(cfg)
+    om.forward(m, full, np.concatenate([toks, [9, a1, a2]]))
+    for l in range(cfg.n_layers):
+        assert np.allclose(s.cache.k[l], full.k[l], rtol=0, atol=1e-12)
+        assert np.allclose(s.cache.v[l], full.v[l], rtol=0, atol=1e-12)
+
+
+def test_greedy_perfect_drafter_multi_round():
+    cfg = tiny()
+    m = om.Model(cfg, 1)
+    s = _session(cfg, m, ctx=10)
+    pending = 3
+    for rnd in range(1, 4):
+        # perfect drafter: the target's greedy continuation
+        c = s.cache.copy()
+        seq = [pending]
+        for _ in range(4):
+            z, _, _ = om.forward(m, c.copy(), seq)
+            seq.append(int(np.argmax(z[-1])))
+        out = verify_step(m, s, rnd, pending, seq[1:], None, exit_layer=1)
+        assert out.final.accepted == 4
+        pending = out.final.tokens[-1]
+    assert s.cache.length == 10 + 3 * 5
+
+
+def test_protocol_errors_leave_session_unchanged():
+    cfg = tiny()
+    m = om.Model(cfg, 1)
+    s = _session(cfg, m, ctx=12, prefill=False)
+    q = np.full((2, cfg.vocab), 1.0 / cfg.vocab)
+    q[1, 5] = 0.0
+    out = verify_step(m, s, 1, 1, [2, 5], q, exit_layer=1)
+    # x_2 = 5 has q = 0: the whole request is a protocol error, KV not advanced
+    assert out.final.status == acc.E_PROTOCOL
+    assert s.cache.length == 12 and s.last_round == 0
+    bad = verify_step(m, s, 5, 1, [2, 3], None)               # round 5 is not the successor of 0
+    assert bad.final.status == acc.E_PROTOCOL and s.cache.length == 12
+    ok = verify_step(m, s, 1, 1, [2, 3], None)
+    assert ok.final.status == acc.OK and s.cache.length == 12 + 1 + ok.final.accepted
