@@ -1,0 +1,204 @@
+/*
+ * sv.h — C ABI of the B200-native verify step of arXiv 2505.21594
+ * ("speculative edge-cloud decoding with early exits").
+ *
+ * The library implements the server side of the paper's Draft-and-Verify loop:
+ *   Verify(M_q, x_{t:t+gamma}, p_{t:t+gamma}) -> x_{t:t+delta+1}     (Eq. 2)
+ * run by a target model with an early exit (Eq. 5), i.e. one
+ * Llama-style decoder pass over the gamma+1 query tokens [pending, x_1..x_gamma]
+ * against a paged KV cache (Eq. 3), an early-exit head
+ * (final RMSNorm + LM head) at layer `exit_layer`,
+ * Leviathan speculative-sampling acceptance (adopted by PAPER.md:24, :80) at the
+ * exit and at the final layer, and KV rollback to the accepted length.
+ *
+ * Letters: p = TARGET distribution, q = DRAFT distribution (the north star's
+ * convention; PAPER.md uses the opposite letters, R1).
+ *
+ * Conventions for every call:
+ *  - plain C, no exceptions cross the ABI; every call returns sv_status;
+ *  - "device" pointers are CUDA device memory of the engine's device (allocated
+ *    by the caller, e.g. with torch); "host" pointers are ordinary or pinned host
+ *    memory; each argument says which;
+ *  - on failure sv_last_error() returns a thread-local message for the last
+ *    failing call on that thread;
+ *  - there is no CPU fallback: on a machine without an sm_100 device every call
+ *    that needs the GPU returns SV_E_DEVICE.
+ */
+#ifndef SV_H_
+#define SV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SV_API __attribute__((visibility("default")))
+#else
+#define SV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SV_MAX_GAMMA 8
+#define SV_ABI_VERSION 1
+
+typedef enum {
+    SV_OK = 0,
+    SV_E_INVALID = 1,   /* bad argument (synchronous)                                   */
+    SV_E_PROTOCOL = 2,  /* per request: drafted token with q_j(x_j) <= 0, or
+                           round_id not the successor / prefix_len != cached_len + 1
+                           (SPEC.md:284); that request's KV is not advanced             */
+    SV_E_CAPACITY = 3,  /* KV pool or engine limits exhausted                           */
+    SV_E_DEVICE = 4,    /* no sm_100 device, or a CUDA error (the engine is poisoned)   */
+    SV_E_BUSY = 5,      /* a ticket is already in flight on this engine                 */
+    SV_E_TIMEOUT = 6    /* sv_wait_* timed out (the ticket is still valid)              */
+} sv_status;
+
+SV_API const char* sv_status_str(sv_status s);
+SV_API const char* sv_last_error(void);
+SV_API int sv_abi_version(void);
+
+/* ---------------------------------------------------------------- model ---- */
+
+/* Llama-style decoder shape.  The paper names only "Llama2-7B";
+ * constants follow HF Llama-2 (R6).  Constraints: d_model % 128 == 0,
+ * head_dim in {32, 64, 128}, n_heads * head_dim == d_model, d_ff % 64 == 0,
+ * vocab % 128 == 0, page_tokens == 64, max_ctx % page_tokens == 0. */
+typedef struct {
+    int32_t n_layers, d_model, n_heads, head_dim, d_ff, vocab, max_ctx, page_tokens;
+    float rms_eps;      /* 1e-5  */
+    float rope_theta;   /* 1e4   */
+} sv_model_cfg;
+
+/* Weight pointers (device, bf16, row-major, caller-owned; must outlive the engine).
+ *   embed      [vocab][d]                      h^(0) = embed[token]           (Eq. 3)
+ *   lm_head    [vocab][d]   norm_final [d]     z = (RMSNorm(h) * norm_final) lm_head^T
+ *   w_qkv[l]   [3d][d]      rows 0..d-1 = W_q, d..2d-1 = W_k, 2d..3d-1 = W_v
+ *   w_o[l]     [d][d]
+ *   w_gu[l]    [2*d_ff][d]  64-row interleave: physical rows 128t..128t+63 are
+ *                           W_gate rows 64t..64t+63, rows 128t+64..128t+127 are
+ *                           W_up rows 64t..64t+63 (so one 128-row GEMM tile
+ *                           holds matching gate/up rows for the SwiGLU epilogue)
+ *   w_down[l]  [d][d_ff]
+ *   norm_attn[l], norm_mlp[l]  [d]  RMSNorm gains                               */
+typedef struct {
+    void* embed;
+    void* lm_head;
+    void* norm_final;
+    void** w_qkv;
+    void** w_o;
+    void** w_gu;
+    void** w_down;
+    void** norm_attn;
+    void** norm_mlp;
+} sv_weights;
+
+/* Bytes of every weight tensor (host out params, any may be NULL). */
+SV_API sv_status sv_weight_sizes(const sv_model_cfg* cfg, size_t* embed, size_t* lm_head,
+                          size_t* norm, size_t* qkv, size_t* o, size_t* gu, size_t* down);
+
+/* Fill all weights with the counter-hash random init (DESIGN.md "Input recipe",
+ * bit-identical to oracle/gen.py).  `stream` is a cudaStream_t (NULL = legacy
+ * default stream); asynchronous. */
+SV_API sv_status sv_weights_generate(const sv_model_cfg* cfg, const sv_weights* w, uint64_t seed,
+                              void* stream);
+
+/* Bytes of one KV block: page_tokens positions of K and V for every layer
+ * (layout DESIGN.md "Data layout in HBM": [layer][K|V][head][slot][head_dim] bf16). */
+SV_API size_t sv_kv_block_bytes(const sv_model_cfg* cfg);
+
+/* --------------------------------------------------------------- engine ---- */
+
+typedef struct sv_engine sv_engine;
+typedef struct sv_session sv_session;
+typedef struct sv_ticket sv_ticket;
+
+typedef struct {
+    int32_t max_batch;   /* max requests per submit (>= 1)                          */
+    int32_t max_gamma;   /* max draft length per submit (1..SV_MAX_GAMMA)           */
+    int32_t use_graphs;  /* 1: replay one CUDA graph per (batch, gamma, exit, ctx)  */
+} sv_engine_opts;
+
+/* kv_pool: device memory (caller-owned, >= one KV block), carved into blocks of
+ * sv_kv_block_bytes().  Returns SV_E_DEVICE if `device` is not compute capability
+ * 10.0 (sm_100a); there is no fallback. */
+SV_API sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights* w, const sv_engine_opts* opts,
+                           int device, void* kv_pool, size_t kv_pool_bytes, sv_engine** out);
+SV_API sv_status sv_engine_destroy(sv_engine* e);
+/* Kernels the last submit launched (graph nodes counted individually). */
+SV_API sv_status sv_engine_last_launches(const sv_engine* e, int32_t* n_kernels);
+
+/* A session is one client's KV cache.  philox_seed keys its random stream
+ * (Philox4x32-10, counter = (element/4, row|purpose<<8, round_id, session_id)). */
+SV_API sv_status sv_session_open(sv_engine* e, uint64_t session_id, uint64_t philox_seed, sv_session** out);
+/* Synthetic KV for positions 0..len-1 (counter-hash bf16, sd 1; oracle/gen.py
+ * synthetic_kv), sets the cached length to len.  Synchronous. */
+SV_API sv_status sv_session_fill_kv(sv_session* s, int32_t len, uint64_t kv_seed);
+SV_API sv_status sv_session_len(const sv_session* s, int32_t* len);
+SV_API sv_status sv_session_close(sv_session* s);
+
+/* ---------------------------------------------------------------- verify ---- */
+
+typedef struct {
+    sv_session* session;
+    uint32_t round_id;            /* must be the session's last round + 1          */
+    int32_t prefix_len;           /* tokens the client holds incl. pending
+                                     (= cached_len + 1), else SV_E_PROTOCOL        */
+    int32_t pending_token;        /* last verified token; its KV is written here   */
+    int32_t gamma;                /* 1..max_gamma, equal for all requests of a submit */
+    const int32_t* draft_tokens;  /* host [gamma]: x_1..x_gamma                     */
+    const float* draft_probs;     /* [gamma][vocab] fp32, row j-1 = q_j; NULL => greedy */
+    int32_t probs_on_host;        /* 0: draft_probs is a device pointer, 1: host    */
+} sv_verify_req;
+
+typedef struct {
+    uint32_t round_id;
+    int32_t exit_layer;           /* layer the result was read at (L = final)      */
+    int32_t is_final;
+    int32_t status;               /* sv_status of this request                     */
+    int32_t accepted;             /* delta in [0, gamma]                           */
+    int32_t tokens[SV_MAX_GAMMA + 1]; /* tokens[0..delta-1] = x_1..x_delta; tokens[delta] = next */
+    float score;                  /* max_{r<=delta} max_v p_r(v)  (Eq. 4; Alg-S s^(i)) */
+    float next_prob;              /* p_delta(tokens[delta])                        */
+    float min_margin;             /* smallest decision margin on the decision path  */
+    int32_t new_len;              /* cached length after the step (final only)     */
+} sv_exit_result;
+
+/* Launch one verify step for n requests (asynchronous, on `stream`).
+ * exit_layer: 0 = no early exit, else 1..n_layers; its result is written to
+ * early[] mid-pass.  early / final_: host arrays [n] (any host memory), valid
+ * after sv_wait_early / sv_wait_final.  The request arrays and host probs must
+ * stay valid until sv_wait_final returns.  One ticket in flight per engine. */
+SV_API sv_status sv_verify_submit(sv_engine* e, const sv_verify_req* reqs, int32_t n, int32_t exit_layer,
+                           sv_exit_result* early, sv_exit_result* final_, void* stream,
+                           sv_ticket** out);
+SV_API sv_status sv_wait_early(sv_ticket* t, int64_t timeout_us);
+SV_API sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us);   /* KV already rolled back */
+SV_API sv_status sv_ticket_release(sv_ticket* t);
+
+/* The north star's synchronous form: verify(draft_tokens, draft_probs, kv) ->
+ * accepted_len, early_exit_token, next_token, for one request. */
+SV_API sv_status sv_verify(sv_session* s, const sv_verify_req* req, int32_t exit_layer,
+                    sv_exit_result* early, sv_exit_result* final_);
+
+/* ----------------------------------------------------------- test hooks ---- */
+
+/* Copy the fp32 logits of the ticket's step: which 0 = exit, 1 = final;
+ * dst: device [n][gamma+1][vocab].  Valid until the next submit. */
+SV_API sv_status sv_debug_logits(sv_ticket* t, int32_t which, float* dst_device);
+/* Run only the acceptance kernels on caller logits (device [n][gamma+1][vocab]);
+ * sessions supply seeds / ids, nothing is committed.  Synchronous. */
+SV_API sv_status sv_debug_accept(sv_engine* e, const float* logits_dev, const sv_verify_req* reqs,
+                          int32_t n, sv_exit_result* out);
+/* Copy cached K and V rows first..first+count-1 of one layer to host
+ * (bf16 [count][d_model], element [pos][head*head_dim + dim]).  Synchronous. */
+SV_API sv_status sv_debug_kv_rows(sv_session* s, int32_t layer, int32_t first, int32_t count,
+                           void* k_host, void* v_host);
+/* Philox4x32-10 evaluated on the device (host in/out).  Synchronous. */
+SV_API sv_status sv_debug_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SV_H_ */

@@ -88,14 +88,35 @@ def gen_bits(seed: int, tid: int, n: int, sd: float, offset: float = 0.0, start:
     return bf16_rne_bits(v)
 
 
+_POOL = None
+
+
+def _pool():
+    """Thread pool over element chunks (numpy releases the GIL inside ufuncs);
+    the values do not depend on the chunking (each element is a pure function
+    of its index)."""
+    global _POOL
+    if _POOL is None:
+        import concurrent.futures as cf
+        import os
+        _POOL = cf.ThreadPoolExecutor(max_workers=max(1, min(64, os.cpu_count() or 1)))
+    return _POOL
+
+
 def gen_tensor(seed: int, tid: int, shape, sd: float, offset: float = 0.0) -> np.ndarray:
     """float64 values (exactly the bf16 numbers) of a whole tensor, row-major."""
     n = int(np.prod(shape))
     out = np.empty(n, dtype=np.float64)
-    chunk = 1 << 24
-    for s0 in range(0, n, chunk):
+    chunk = 1 << 21
+
+    def work(s0):
         m = min(chunk, n - s0)
         out[s0:s0 + m] = bf16_bits_to_f64(gen_bits(seed, tid, m, sd, offset, start=s0))
+
+    if n <= chunk:
+        work(0)
+    else:
+        list(_pool().map(work, range(0, n, chunk)))
     return out.reshape(shape)
 
 

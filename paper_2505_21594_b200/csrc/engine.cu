@@ -1,0 +1,910 @@
+// engine.cu — the C ABI of include/sv.h: engine, sessions, paged-KV block
+// allocator, step orchestration (two streams: main + early-exit fork), CUDA-graph
+// cache and result mailboxes.
+//
+// One verify step, issued as one graph:
+//   K4 embed
+//   for each layer l: K1 QKV(+RMSNorm fold, RoPE, KV append) -> K3 attention
+//                     -> K1 O(+residual) -> K1 gate/up(+SwiGLU) -> K1 down(+residual)
+//   after layer l_e : fork to the exit stream: K1 LM head -> K5 accept -> D2H
+//                     of the early result + a sequence flag (mid-pass delivery)
+//   after layer L   : K1 LM head -> K5 accept + K6 rollback -> D2H final result
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "../../include/sv.h"
+#include "kernels.h"
+
+using namespace sv;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static sv_status fail(sv_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t _e = (call);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            return fail(SV_E_DEVICE, std::string(#call " -> ") + cudaGetErrorString(_e));     \
+    } while (0)
+
+extern "C" const char* sv_status_str(sv_status s) {
+    switch (s) {
+        case SV_OK: return "SV_OK";
+        case SV_E_INVALID: return "SV_E_INVALID";
+        case SV_E_PROTOCOL: return "SV_E_PROTOCOL";
+        case SV_E_CAPACITY: return "SV_E_CAPACITY";
+        case SV_E_DEVICE: return "SV_E_DEVICE";
+        case SV_E_BUSY: return "SV_E_BUSY";
+        case SV_E_TIMEOUT: return "SV_E_TIMEOUT";
+    }
+    return "SV_E_UNKNOWN";
+}
+extern "C" const char* sv_last_error(void) { return g_err.c_str(); }
+extern "C" int sv_abi_version(void) { return SV_ABI_VERSION; }
+
+// ------------------------------------------------------------------ helpers
+static const double IH_SD = std::sqrt(21845.0);
+static float gen_scale(double sd) { return (float)(sd / IH_SD); }
+
+static sv_status check_cfg(const sv_model_cfg* c) {
+    if (!c) return fail(SV_E_INVALID, "cfg is NULL");
+    if (c->n_layers < 1 || c->d_model <= 0 || c->d_model % 128 || c->n_heads <= 0 ||
+        c->n_heads * c->head_dim != c->d_model || !(c->head_dim == 32 || c->head_dim == 64 || c->head_dim == 128) ||
+        c->d_ff <= 0 || c->d_ff % 64 || c->vocab <= 0 || c->vocab % 128 || c->page_tokens != 64 ||
+        c->max_ctx <= 0 || c->max_ctx % c->page_tokens)
+        return fail(SV_E_INVALID, "unsupported model shape (see sv_model_cfg constraints)");
+    return SV_OK;
+}
+
+static sv_status require_sm100(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(SV_E_DEVICE, "no CUDA device (no CPU fallback)");
+    if (device < 0 || device >= n) return fail(SV_E_DEVICE, "bad device ordinal");
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return fail(SV_E_DEVICE, "cudaGetDeviceProperties failed");
+    if (p.major != 10 || p.minor != 0)
+        return fail(SV_E_DEVICE, "device is not sm_100 (B200); this library has no other code path");
+    return SV_OK;
+}
+
+extern "C" sv_status sv_weight_sizes(const sv_model_cfg* c, size_t* embed, size_t* lm_head, size_t* norm,
+                                     size_t* qkv, size_t* o, size_t* gu, size_t* down) {
+    sv_status s = check_cfg(c);
+    if (s) return s;
+    const size_t d = c->d_model, F = c->d_ff, V = c->vocab;
+    if (embed) *embed = V * d * 2;
+    if (lm_head) *lm_head = V * d * 2;
+    if (norm) *norm = d * 2;
+    if (qkv) *qkv = 3 * d * d * 2;
+    if (o) *o = d * d * 2;
+    if (gu) *gu = 2 * F * d * 2;
+    if (down) *down = d * F * 2;
+    return SV_OK;
+}
+
+extern "C" size_t sv_kv_block_bytes(const sv_model_cfg* c) {
+    if (check_cfg(c)) return 0;
+    return (size_t)c->n_layers * 2 * c->d_model * c->page_tokens * 2;
+}
+
+// tensor ids of the generator (oracle/gen.py documents the same numbering)
+enum { TID_EMBED = 1, TID_LM_HEAD = 2, TID_NORM_FINAL = 3 };
+static uint64_t layer_tid(int l, int kind) { return 16 + 16 * (uint64_t)l + kind; }
+
+extern "C" sv_status sv_weights_generate(const sv_model_cfg* c, const sv_weights* w, uint64_t seed, void* stream) {
+    sv_status s = check_cfg(c);
+    if (s) return s;
+    if (!w) return fail(SV_E_INVALID, "weights is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int d = c->d_model, F = c->d_ff, V = c->vocab, L = c->n_layers;
+    const double s_in = 1.28 / std::sqrt((double)d);
+    const double s_out = s_in / std::sqrt(2.0 * L);
+    CK(gen_launch(w->embed, (uint64_t)V * d, GEN_PLAIN, seed, TID_EMBED, 0, d, gen_scale(1.0), 0.f, st));
+    CK(gen_launch(w->lm_head, (uint64_t)V * d, GEN_PLAIN, seed, TID_LM_HEAD, 0, d, gen_scale(3.2 / std::sqrt((double)d)),
+                  0.f, st));
+    CK(gen_launch(w->norm_final, d, GEN_PLAIN, seed, TID_NORM_FINAL, 0, d, gen_scale(0.1), 1.0f, st));
+    for (int l = 0; l < L; ++l) {
+        CK(gen_launch(w->w_qkv[l], (uint64_t)3 * d * d, GEN_QKV, seed, layer_tid(l, 0), d, d, gen_scale(s_in), 0.f, st));
+        CK(gen_launch(w->w_o[l], (uint64_t)d * d, GEN_PLAIN, seed, layer_tid(l, 3), 0, d, gen_scale(s_out), 0.f, st));
+        CK(gen_launch(w->w_gu[l], (uint64_t)2 * F * d, GEN_GU, seed, layer_tid(l, 4), 0, d, gen_scale(s_in), 0.f, st));
+        CK(gen_launch(w->w_down[l], (uint64_t)d * F, GEN_PLAIN, seed, layer_tid(l, 6), 0, F, gen_scale(s_out), 0.f, st));
+        CK(gen_launch(w->norm_attn[l], d, GEN_PLAIN, seed, layer_tid(l, 7), 0, d, gen_scale(0.1), 1.0f, st));
+        CK(gen_launch(w->norm_mlp[l], d, GEN_PLAIN, seed, layer_tid(l, 8), 0, d, gen_scale(0.1), 1.0f, st));
+    }
+    return SV_OK;
+}
+
+// ------------------------------------------------------------------ engine
+struct sv_session {
+    sv_engine* e;
+    uint64_t id, seed;
+    std::vector<int32_t> blocks;
+    int32_t len = 0;
+    uint32_t last_round = 0;
+    bool busy = false;
+};
+
+struct StepKey {
+    int n, gamma, exit_layer, nchunk;
+    bool operator<(const StepKey& o) const {
+        return std::tie(n, gamma, exit_layer, nchunk) < std::tie(o.n, o.gamma, o.exit_layer, o.nchunk);
+    }
+};
+
+struct sv_ticket {
+    sv_engine* e;
+    int n;
+    std::vector<int> gpu_slot;                   // request i -> batch slot (or -1)
+    std::vector<sv_status> host_status;          // host-detected status per request
+    std::vector<sv_session*> sess;
+    std::vector<uint32_t> rounds;
+    std::vector<int32_t> ctx;
+    sv_exit_result* early;
+    sv_exit_result* final_;
+    int exit_layer;
+    uint64_t seq;
+    int nb = 0, gamma = 0;
+    bool has_gpu;
+    bool early_done = false, final_done = false;
+    cudaEvent_t ev_done;
+};
+
+struct sv_engine {
+    sv_model_cfg cfg;
+    sv_engine_opts opts;
+    int device, num_sms;
+    // weights
+    void *embed, *lm_head, *norm_final;
+    std::vector<void*> w_qkv, w_o, w_gu, w_down, norm_attn, norm_mlp;
+    // KV pool
+    uint8_t* kv_pool;
+    size_t blk_bytes;
+    int nblocks;
+    std::vector<int32_t> free_blocks;
+    int pt_stride;
+    // sizes
+    int max_rows, MP, d, F, V, L, H, D;
+    // device scratch
+    float *h, *qbuf, *ssq, *logits_exit, *logits_final, *ws_main, *ws_exit, *rope, *attn_o, *attn_ml;
+    bf16_raw_t *u, *u_exit, *attn_out, *act;
+    int *cnt_main, *cnt_exit, *cnt_attn, *cnt_acc_exit, *cnt_acc_final;
+    RowStat *stats_exit, *stats_final;
+    RacePart *race_exit, *race_final;
+    sv_exit_result *res_exit_dev, *res_final_dev;
+    size_t ws_elems;
+    int acc_nch, acc_chunk, max_nchunk;
+    float* probs_stage = nullptr;               // device copy of host draft probs
+    // per-step metadata (device + pinned staging, same layout)
+    uint8_t *meta_dev, *meta_host;
+    size_t meta_bytes, off_tok, off_pos, off_req, off_ctx, off_pt, off_reqdev, off_seq;
+    // pinned mailboxes
+    sv_exit_result *mb_exit, *mb_final;
+    volatile uint64_t* mb_flag;
+    // tensor maps
+    std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;
+    CUtensorMap tm_lm;
+    std::map<int, std::vector<CUtensorMap>> tm_act;   // tile_n -> {u, attn_out, act, u_exit}
+    // streams / graphs
+    cudaStream_t s_cap, s_exit;
+    cudaEvent_t ev_fork, ev_join;
+    std::map<StepKey, cudaGraphExec_t> graphs;
+    int last_launches = 0;
+    uint64_t seq = 0;
+    sv_ticket* inflight = nullptr;
+    bool poisoned = false;
+    std::mutex mu;
+};
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static sv_status engine_alloc(sv_engine* e) {
+    const int d = e->d, F = e->F, V = e->V, MP = e->MP;
+    auto dalloc = [&](void** p, size_t bytes) -> cudaError_t {
+        cudaError_t r = cudaMalloc(p, bytes);
+        if (r == cudaSuccess) r = cudaMemset(*p, 0, bytes);
+        return r;
+    };
+    CK(dalloc((void**)&e->h, (size_t)MP * d * 4));
+    CK(dalloc((void**)&e->qbuf, (size_t)MP * d * 4));
+    CK(dalloc((void**)&e->ssq, (size_t)(2 * e->L + 1) * (d / 128) * MP * 4));
+    CK(dalloc((void**)&e->logits_exit, (size_t)MP * V * 4));
+    CK(dalloc((void**)&e->logits_final, (size_t)MP * V * 4));
+    CK(dalloc((void**)&e->u, (size_t)MP * d * 2));
+    CK(dalloc((void**)&e->u_exit, (size_t)MP * d * 2));
+    CK(dalloc((void**)&e->attn_out, (size_t)MP * d * 2));
+    CK(dalloc((void**)&e->act, (size_t)MP * F * 2));
+    // split-K workspace: the largest splits * tiles * MP * 128 over all GEMMs and row counts
+    size_t ws = 128;
+    const int shapes[5][2] = {{3 * d, d}, {d, d}, {2 * F, d}, {d, F}, {V, d}};
+    for (int M = 1; M <= e->max_rows; ++M) {
+        const int tn = gemm_pick_tile_n(M);
+        for (auto& s : shapes) {
+            const int sp = gemm_pick_splits(s[0], s[1], M, tn, e->num_sms);
+            if (sp > 1) ws = std::max(ws, (size_t)sp * (s[0] / 128) * MP * 128);
+        }
+    }
+    e->ws_elems = ws;
+    CK(dalloc((void**)&e->ws_main, ws * 4));
+    CK(dalloc((void**)&e->ws_exit, ws * 4));
+    const int max_tiles = std::max({3 * d, 2 * F, V}) / 128 * (MP / 16 + 1);
+    CK(dalloc((void**)&e->cnt_main, (size_t)max_tiles * 4));
+    CK(dalloc((void**)&e->cnt_exit, (size_t)max_tiles * 4));
+    // attention partials
+    e->max_nchunk = e->cfg.max_ctx / 64 + 1;
+    const size_t bh = (size_t)e->opts.max_batch * e->H;
+    const int G = e->opts.max_gamma + 1;
+    CK(dalloc((void**)&e->attn_o, bh * e->max_nchunk * G * e->D * 4));
+    CK(dalloc((void**)&e->attn_ml, bh * e->max_nchunk * G * 2 * 4));
+    CK(dalloc((void**)&e->cnt_attn, bh * 4));
+    // acceptance
+    e->acc_nch = accept_chunks(V, &e->acc_chunk);
+    CK(dalloc((void**)&e->stats_exit, (size_t)e->max_rows * e->acc_nch * sizeof(RowStat)));
+    CK(dalloc((void**)&e->stats_final, (size_t)e->max_rows * e->acc_nch * sizeof(RowStat)));
+    CK(dalloc((void**)&e->race_exit, (size_t)e->opts.max_batch * e->acc_nch * sizeof(RacePart)));
+    CK(dalloc((void**)&e->race_final, (size_t)e->opts.max_batch * e->acc_nch * sizeof(RacePart)));
+    CK(dalloc((void**)&e->cnt_acc_exit, (size_t)e->opts.max_batch * 4));
+    CK(dalloc((void**)&e->cnt_acc_final, (size_t)e->opts.max_batch * 4));
+    CK(dalloc((void**)&e->res_exit_dev, (size_t)e->opts.max_batch * sizeof(sv_exit_result)));
+    CK(dalloc((void**)&e->res_final_dev, (size_t)e->opts.max_batch * sizeof(sv_exit_result)));
+    // RoPE table (cos, sin) in double -> fp32: angle = pos * theta^(-2i/Dh)
+    {
+        const int half = e->D / 2, npos = e->cfg.max_ctx + 16;
+        std::vector<float> t((size_t)npos * half * 2);
+        for (int p = 0; p < npos; ++p)
+            for (int i = 0; i < half; ++i) {
+                const double ang = (double)p * std::pow((double)e->cfg.rope_theta, -2.0 * i / e->D);
+                t[((size_t)p * half + i) * 2 + 0] = (float)std::cos(ang);
+                t[((size_t)p * half + i) * 2 + 1] = (float)std::sin(ang);
+            }
+        CK(dalloc((void**)&e->rope, t.size() * 4));
+        CK(cudaMemcpy(e->rope, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+    }
+    // metadata block
+    const int B = e->opts.max_batch;
+    size_t off = 0;
+    e->off_tok = off; off = align_up(off + (size_t)MP * 4, 256);
+    e->off_pos = off; off = align_up(off + (size_t)MP * 4, 256);
+    e->off_req = off; off = align_up(off + (size_t)MP * 4, 256);
+    e->off_ctx = off; off = align_up(off + (size_t)B * 4, 256);
+    e->off_pt = off; off = align_up(off + (size_t)B * e->pt_stride * 4, 256);
+    e->off_reqdev = off; off = align_up(off + (size_t)B * sizeof(ReqDev), 256);
+    e->off_seq = off; off = align_up(off + 8, 256);
+    e->meta_bytes = off;
+    CK(dalloc((void**)&e->meta_dev, off));
+    CK(cudaMallocHost((void**)&e->meta_host, off));
+    memset(e->meta_host, 0, off);
+    CK(cudaMallocHost((void**)&e->mb_exit, (size_t)B * sizeof(sv_exit_result)));
+    CK(cudaMallocHost((void**)&e->mb_final, (size_t)B * sizeof(sv_exit_result)));
+    CK(cudaMallocHost((void**)&e->mb_flag, 64));
+    *e->mb_flag = 0;
+    return SV_OK;
+}
+
+static sv_status engine_tmaps(sv_engine* e) {
+    const int d = e->d, F = e->F;
+    e->tm_qkv.resize(e->L); e->tm_o.resize(e->L); e->tm_gu.resize(e->L); e->tm_down.resize(e->L);
+    for (int l = 0; l < e->L; ++l) {
+        if (!make_tmap_bf16(&e->tm_qkv[l], e->w_qkv[l], 3 * d, d, 128) ||
+            !make_tmap_bf16(&e->tm_o[l], e->w_o[l], d, d, 128) ||
+            !make_tmap_bf16(&e->tm_gu[l], e->w_gu[l], 2 * F, d, 128) ||
+            !make_tmap_bf16(&e->tm_down[l], e->w_down[l], d, F, 128))
+            return fail(SV_E_DEVICE, "cuTensorMapEncodeTiled failed (weights)");
+    }
+    if (!make_tmap_bf16(&e->tm_lm, e->lm_head, e->V, d, 128)) return fail(SV_E_DEVICE, "tensor map (lm_head)");
+    for (int tn : {16, 32, 64, 128, 256}) {
+        if (tn > e->MP) continue;
+        std::vector<CUtensorMap> m(4);
+        if (!make_tmap_bf16(&m[0], e->u, e->MP, d, tn) || !make_tmap_bf16(&m[1], e->attn_out, e->MP, d, tn) ||
+            !make_tmap_bf16(&m[2], e->act, e->MP, F, tn) || !make_tmap_bf16(&m[3], e->u_exit, e->MP, d, tn))
+            return fail(SV_E_DEVICE, "tensor map (activations)");
+        e->tm_act[tn] = m;
+    }
+    return SV_OK;
+}
+
+extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights* w, const sv_engine_opts* opts,
+                                      int device, void* kv_pool, size_t kv_pool_bytes, sv_engine** out) {
+    sv_status s = check_cfg(cfg);
+    if (s) return s;
+    if (!w || !opts || !out || !kv_pool) return fail(SV_E_INVALID, "NULL argument");
+    if (opts->max_batch < 1 || opts->max_gamma < 1 || opts->max_gamma > SV_MAX_GAMMA)
+        return fail(SV_E_INVALID, "bad engine options");
+    if ((s = require_sm100(device))) return s;
+    CK(cudaSetDevice(device));
+    sv_engine* e = new sv_engine();
+    e->cfg = *cfg;
+    e->opts = *opts;
+    e->device = device;
+    CK(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device));
+    e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
+    e->L = cfg->n_layers; e->d = cfg->d_model; e->F = cfg->d_ff; e->V = cfg->vocab;
+    e->H = cfg->n_heads; e->D = cfg->head_dim;
+    for (int l = 0; l < e->L; ++l) {
+        e->w_qkv.push_back(w->w_qkv[l]); e->w_o.push_back(w->w_o[l]); e->w_gu.push_back(w->w_gu[l]);
+        e->w_down.push_back(w->w_down[l]); e->norm_attn.push_back(w->norm_attn[l]); e->norm_mlp.push_back(w->norm_mlp[l]);
+    }
+    e->blk_bytes = sv_kv_block_bytes(cfg);
+    e->kv_pool = (uint8_t*)kv_pool;
+    e->nblocks = (int)(kv_pool_bytes / e->blk_bytes);
+    if (e->nblocks < 1) { delete e; return fail(SV_E_CAPACITY, "kv pool smaller than one block"); }
+    for (int i = e->nblocks - 1; i >= 0; --i) e->free_blocks.push_back(i);
+    e->pt_stride = cfg->max_ctx / cfg->page_tokens + 1;
+    e->max_rows = opts->max_batch * (opts->max_gamma + 1);
+    e->MP = (int)align_up((size_t)e->max_rows, 256);
+    if ((s = engine_alloc(e)) || (s = engine_tmaps(e))) {
+        delete e;
+        return s;
+    }
+    CK(cudaStreamCreateWithFlags(&e->s_cap, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&e->s_exit, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
+    *out = e;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_engine_destroy(sv_engine* e) {
+    if (!e) return fail(SV_E_INVALID, "NULL engine");
+    cudaSetDevice(e->device);
+    cudaDeviceSynchronize();
+    for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
+    void* dev[] = {e->h, e->qbuf, e->ssq, e->logits_exit, e->logits_final, e->ws_main, e->ws_exit, e->rope,
+                   e->attn_o, e->attn_ml, e->u, e->u_exit, e->attn_out, e->act, e->cnt_main, e->cnt_exit,
+                   e->cnt_attn, e->cnt_acc_exit, e->cnt_acc_final, e->stats_exit, e->stats_final, e->race_exit,
+                   e->race_final, e->res_exit_dev, e->res_final_dev, e->meta_dev, e->probs_stage};
+    for (void* p : dev)
+        if (p) cudaFree(p);
+    cudaFreeHost(e->meta_host);
+    cudaFreeHost(e->mb_exit);
+    cudaFreeHost(e->mb_final);
+    cudaFreeHost((void*)e->mb_flag);
+    cudaStreamDestroy(e->s_cap);
+    cudaStreamDestroy(e->s_exit);
+    cudaEventDestroy(e->ev_fork);
+    cudaEventDestroy(e->ev_join);
+    delete e;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_engine_last_launches(const sv_engine* e, int32_t* n) {
+    if (!e || !n) return fail(SV_E_INVALID, "NULL argument");
+    *n = e->last_launches;
+    return SV_OK;
+}
+
+// ------------------------------------------------------------------ sessions
+static bool ensure_blocks(sv_engine* e, sv_session* s, int len) {
+    const int need = (len + e->cfg.page_tokens - 1) / e->cfg.page_tokens;
+    while ((int)s->blocks.size() < need) {
+        if (e->free_blocks.empty()) return false;
+        s->blocks.push_back(e->free_blocks.back());
+        e->free_blocks.pop_back();
+    }
+    return true;
+}
+
+extern "C" sv_status sv_session_open(sv_engine* e, uint64_t session_id, uint64_t philox_seed, sv_session** out) {
+    if (!e || !out) return fail(SV_E_INVALID, "NULL argument");
+    sv_session* s = new sv_session();
+    s->e = e;
+    s->id = session_id;
+    s->seed = philox_seed;
+    *out = s;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_session_fill_kv(sv_session* s, int32_t len, uint64_t kv_seed) {
+    if (!s) return fail(SV_E_INVALID, "NULL session");
+    sv_engine* e = s->e;
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (s->busy) return fail(SV_E_BUSY, "session has a ticket in flight");
+    if (len < 0 || len + SV_MAX_GAMMA + 1 > e->cfg.max_ctx) return fail(SV_E_INVALID, "len out of range");
+    if (!ensure_blocks(e, s, std::max(len, 1))) return fail(SV_E_CAPACITY, "KV pool exhausted");
+    CK(cudaSetDevice(e->device));
+    int32_t* dblocks = nullptr;
+    CK(cudaMalloc(&dblocks, s->blocks.size() * 4));
+    CK(cudaMemcpy(dblocks, s->blocks.data(), s->blocks.size() * 4, cudaMemcpyHostToDevice));
+    CK(kvfill_launch((bf16_raw_t*)e->kv_pool, dblocks, (int)s->blocks.size(), len, kv_seed, e->L, e->H, e->D,
+                     e->cfg.page_tokens, gen_scale(1.0), 0));
+    CK(cudaDeviceSynchronize());
+    CK(cudaFree(dblocks));
+    s->len = len;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_session_len(const sv_session* s, int32_t* len) {
+    if (!s || !len) return fail(SV_E_INVALID, "NULL argument");
+    *len = s->len;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_session_close(sv_session* s) {
+    if (!s) return fail(SV_E_INVALID, "NULL session");
+    sv_engine* e = s->e;
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (s->busy) return fail(SV_E_BUSY, "session has a ticket in flight");
+    for (int b : s->blocks) e->free_blocks.push_back(b);
+    delete s;
+    return SV_OK;
+}
+
+// ------------------------------------------------------------------ one step
+static GemmArgs base_args(sv_engine* e, int M) {
+    GemmArgs a = {};
+    a.M = M;
+    a.MP = e->MP;
+    a.inv_d = 1.0f / e->d;
+    a.eps = e->cfg.rms_eps;
+    a.ssq_tiles = e->d / 128;
+    a.n_layers = e->L; a.n_heads = e->H; a.head_dim = e->D; a.d_model = e->d; a.page_tokens = e->cfg.page_tokens;
+    a.d_ff = e->F;
+    a.rope_cs = e->rope;
+    a.kv_pool = (bf16_raw_t*)e->kv_pool;
+    a.meta.tok = (int32_t*)(e->meta_dev + e->off_tok);
+    a.meta.pos = (int32_t*)(e->meta_dev + e->off_pos);
+    a.meta.row_req = (int32_t*)(e->meta_dev + e->off_req);
+    a.meta.ctx = (int32_t*)(e->meta_dev + e->off_ctx);
+    a.meta.page_table = (int32_t*)(e->meta_dev + e->off_pt);
+    a.meta.pt_stride = e->pt_stride;
+    return a;
+}
+
+static float* ssq_at(sv_engine* e, int layer, int which) {   // norm point (layer, 0 = attn / 1 = mlp)
+    return e->ssq + (size_t)(2 * layer + which) * (e->d / 128) * e->MP;
+}
+
+// Issues every kernel / copy of one step on (main, exit) streams; returns launch count.
+static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk,
+                              int* launches) {
+    const int G = gamma + 1, M = n * G, d = e->d, F = e->F, V = e->V, L = e->L;
+    const int tn = gemm_pick_tile_n(M);
+    const auto& tma = e->tm_act[tn];   // {u, attn_out, act, u_exit}
+    int nl = 0;
+    cudaError_t r;
+#define LAUNCH(x)                         \
+    do {                                  \
+        if ((r = (x)) != cudaSuccess) return r; \
+        ++nl;                             \
+    } while (0)
+
+    EmbedArgs ea{(const int32_t*)(e->meta_dev + e->off_tok), e->embed, e->norm_attn[0], e->h, e->u, ssq_at(e, 0, 0), M,
+                 e->MP, d};
+    LAUNCH(embed_launch(ea, st));
+
+    auto gemm = [&](int epi, const CUtensorMap& A, const CUtensorMap& B, int N, int K, GemmArgs a, cudaStream_t s,
+                    bool exit_ws) -> cudaError_t {
+        a.N = N;
+        a.K = K;
+        a.splits = gemm_pick_splits(N, K, M, tn, e->num_sms);
+        a.ws = exit_ws ? e->ws_exit : e->ws_main;
+        a.counters = exit_ws ? e->cnt_exit : e->cnt_main;
+        return gemm_launch(epi, tn, A, B, a, s);
+    };
+    auto lm_and_accept = [&](cudaStream_t s, bool is_exit) -> cudaError_t {
+        GemmArgs a = base_args(e, M);
+        a.ssq_in = ssq_at(e, is_exit ? exit_layer : L, 0);
+        a.logits = is_exit ? e->logits_exit : e->logits_final;
+        cudaError_t q = gemm(EPI_LOGITS, e->tm_lm, is_exit ? tma[3] : tma[0], V, d, a, s, is_exit);
+        if (q != cudaSuccess) return q;
+        ++nl;
+        AcceptArgs aa = {};
+        aa.logits = a.logits;
+        aa.req = (const ReqDev*)(e->meta_dev + e->off_reqdev);
+        aa.stats = is_exit ? e->stats_exit : e->stats_final;
+        aa.race = is_exit ? e->race_exit : e->race_final;
+        aa.counters = is_exit ? e->cnt_acc_exit : e->cnt_acc_final;
+        aa.out = is_exit ? e->res_exit_dev : e->res_final_dev;
+        aa.B = n; aa.G = G; aa.V = V; aa.nch = e->acc_nch; aa.chunk = e->acc_chunk;
+        aa.exit_layer = is_exit ? exit_layer : L;
+        aa.is_final = is_exit ? 0 : 1;
+        q = accept_launch(aa, s);
+        nl += 2;
+        return q;
+    };
+
+    for (int l = 0; l < L; ++l) {
+        {   // QKV + RoPE + KV append
+            GemmArgs a = base_args(e, M);
+            a.layer = l;
+            a.ssq_in = ssq_at(e, l, 0);
+            a.qbuf = e->qbuf;
+            LAUNCH(gemm(EPI_QKV, e->tm_qkv[l], tma[0], 3 * d, d, a, st, false));
+        }
+        {   // attention
+            AttnArgs aa = {};
+            aa.q = e->qbuf; aa.kv_pool = (const bf16_raw_t*)e->kv_pool; aa.out = e->attn_out;
+            aa.part_o = e->attn_o; aa.part_ml = e->attn_ml; aa.counters = e->cnt_attn;
+            aa.ctx = (const int32_t*)(e->meta_dev + e->off_ctx);
+            aa.page_table = (const int32_t*)(e->meta_dev + e->off_pt);
+            aa.pt_stride = e->pt_stride;
+            aa.B = n; aa.G = G; aa.n_heads = e->H; aa.head_dim = e->D; aa.d_model = d; aa.n_layers = L;
+            aa.layer = l; aa.page_tokens = e->cfg.page_tokens; aa.nchunk = nchunk;
+            aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)e->D));
+            LAUNCH(attn_launch(aa, st));
+        }
+        {   // O projection + residual
+            GemmArgs a = base_args(e, M);
+            a.h = e->h; a.g_out = e->norm_mlp[l]; a.u_out = e->u; a.ssq_out = ssq_at(e, l, 1);
+            LAUNCH(gemm(EPI_RESID, e->tm_o[l], tma[1], d, d, a, st, false));
+        }
+        {   // gate/up + SwiGLU
+            GemmArgs a = base_args(e, M);
+            a.ssq_in = ssq_at(e, l, 1);
+            a.act = e->act;
+            LAUNCH(gemm(EPI_SWIGLU, e->tm_gu[l], tma[0], 2 * F, d, a, st, false));
+        }
+        {   // down + residual (+ early-exit copy with the final gain)
+            GemmArgs a = base_args(e, M);
+            a.h = e->h;
+            a.g_out = (l + 1 < L) ? e->norm_attn[l + 1] : e->norm_final;
+            a.u_out = e->u;
+            if (l + 1 == exit_layer) {
+                a.g_out2 = e->norm_final;
+                a.u_out2 = e->u_exit;
+            }
+            a.ssq_out = ssq_at(e, l + 1, 0);
+            LAUNCH(gemm(EPI_RESID, e->tm_down[l], tma[2], d, F, a, st, false));
+        }
+        if (l + 1 == exit_layer) {   // fork the early exit (S10-S11)
+            if ((r = cudaEventRecord(e->ev_fork, st)) != cudaSuccess) return r;
+            if ((r = cudaStreamWaitEvent(e->s_exit, e->ev_fork, 0)) != cudaSuccess) return r;
+            if ((r = lm_and_accept(e->s_exit, true)) != cudaSuccess) return r;
+            if ((r = cudaMemcpyAsync(e->mb_exit, e->res_exit_dev, (size_t)n * sizeof(sv_exit_result),
+                                     cudaMemcpyDeviceToHost, e->s_exit)) != cudaSuccess)
+                return r;
+            if ((r = cudaMemcpyAsync((void*)e->mb_flag, e->meta_dev + e->off_seq, 8, cudaMemcpyDeviceToHost,
+                                     e->s_exit)) != cudaSuccess)
+                return r;
+            if ((r = cudaEventRecord(e->ev_join, e->s_exit)) != cudaSuccess) return r;
+        }
+    }
+    if ((r = lm_and_accept(st, false)) != cudaSuccess) return r;
+    if ((r = cudaMemcpyAsync(e->mb_final, e->res_final_dev, (size_t)n * sizeof(sv_exit_result), cudaMemcpyDeviceToHost,
+                             st)) != cudaSuccess)
+        return r;
+    if (exit_layer > 0)
+        if ((r = cudaStreamWaitEvent(st, e->ev_join, 0)) != cudaSuccess) return r;
+#undef LAUNCH
+    *launches = nl;
+    return cudaSuccess;
+}
+
+static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk) {
+    CK(cudaMemcpyAsync(e->meta_dev, e->meta_host, e->meta_bytes, cudaMemcpyHostToDevice, st));
+    int nl = 0;
+    if (!e->opts.use_graphs) {
+        CK(issue_step(e, st, n, gamma, exit_layer, nchunk, &nl));
+        e->last_launches = nl;
+        return SV_OK;
+    }
+    StepKey key{n, gamma, exit_layer, nchunk};
+    auto it = e->graphs.find(key);
+    if (it == e->graphs.end()) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(e->s_cap, cudaStreamCaptureModeThreadLocal));
+        cudaError_t r = issue_step(e, e->s_cap, n, gamma, exit_layer, nchunk, &nl);
+        cudaError_t r2 = cudaStreamEndCapture(e->s_cap, &g);
+        if (r != cudaSuccess) return fail(SV_E_DEVICE, std::string("capture: ") + cudaGetErrorString(r));
+        CK(r2);
+        cudaGraphExec_t ex;
+        CK(cudaGraphInstantiate(&ex, g, 0));
+        CK(cudaGraphDestroy(g));
+        it = e->graphs.emplace(key, ex).first;
+        e->last_launches = nl;
+    }
+    CK(cudaGraphLaunch(it->second, st));
+    return SV_OK;
+}
+
+extern "C" sv_status sv_verify_submit(sv_engine* e, const sv_verify_req* reqs, int32_t n, int32_t exit_layer,
+                                      sv_exit_result* early, sv_exit_result* final_, void* stream, sv_ticket** out) {
+    if (!e || !reqs || !final_ || !out || n < 1) return fail(SV_E_INVALID, "bad arguments");
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (e->poisoned) return fail(SV_E_DEVICE, "engine poisoned by an earlier CUDA error");
+    if (e->inflight) return fail(SV_E_BUSY, "a ticket is already in flight on this engine");
+    if (n > e->opts.max_batch) return fail(SV_E_CAPACITY, "n > max_batch");
+    if (exit_layer < 0 || exit_layer > e->L) return fail(SV_E_INVALID, "exit_layer out of range");
+    if (exit_layer > 0 && !early) return fail(SV_E_INVALID, "early result array required when exit_layer > 0");
+    const int gamma = reqs[0].gamma;
+    if (gamma < 1 || gamma > e->opts.max_gamma) return fail(SV_E_INVALID, "gamma out of range");
+    for (int i = 0; i < n; ++i) {
+        const sv_verify_req& q = reqs[i];
+        if (!q.session || q.session->e != e) return fail(SV_E_INVALID, "request without a session of this engine");
+        if (q.gamma != gamma) return fail(SV_E_INVALID, "gamma must be equal for all requests of a submit");
+        if (!q.draft_tokens) return fail(SV_E_INVALID, "draft_tokens is NULL");
+        if (q.pending_token < 0 || q.pending_token >= e->V) return fail(SV_E_INVALID, "pending token out of range");
+        for (int j = 0; j < gamma; ++j)
+            if (q.draft_tokens[j] < 0 || q.draft_tokens[j] >= e->V) return fail(SV_E_INVALID, "draft token out of range");
+        if (q.session->busy) return fail(SV_E_BUSY, "session has a ticket in flight");
+        for (int k = 0; k < i; ++k)
+            if (reqs[k].session == q.session) return fail(SV_E_INVALID, "session twice in one submit");
+    }
+    CK(cudaSetDevice(e->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int G = gamma + 1;
+    sv_ticket* t = new sv_ticket();
+    t->e = e; t->n = n; t->early = early; t->final_ = final_; t->exit_layer = exit_layer;
+    t->gpu_slot.assign(n, -1);
+    t->host_status.assign(n, SV_OK);
+    // S0: validate protocol state, build the batch of valid requests
+    int nb = 0, max_len = 0;
+    uint8_t* mh = e->meta_host;
+    int32_t* tok = (int32_t*)(mh + e->off_tok);
+    int32_t* pos = (int32_t*)(mh + e->off_pos);
+    int32_t* rreq = (int32_t*)(mh + e->off_req);
+    int32_t* ctxa = (int32_t*)(mh + e->off_ctx);
+    int32_t* pt = (int32_t*)(mh + e->off_pt);
+    ReqDev* rd = (ReqDev*)(mh + e->off_reqdev);
+    for (int i = 0; i < n; ++i) {
+        const sv_verify_req& q = reqs[i];
+        sv_session* s = q.session;
+        t->sess.push_back(s);
+        t->rounds.push_back(q.round_id);
+        t->ctx.push_back(s->len);
+        if (q.round_id != s->last_round + 1 || q.prefix_len != s->len + 1) {
+            t->host_status[i] = SV_E_PROTOCOL;
+            continue;
+        }
+        if (s->len + G > e->cfg.max_ctx || !ensure_blocks(e, s, s->len + G)) {
+            t->host_status[i] = SV_E_CAPACITY;
+            continue;
+        }
+        const int b = nb++;
+        t->gpu_slot[i] = b;
+        for (int j = 0; j < G; ++j) {
+            tok[b * G + j] = j == 0 ? q.pending_token : q.draft_tokens[j - 1];
+            pos[b * G + j] = s->len + j;
+            rreq[b * G + j] = b;
+        }
+        ctxa[b] = s->len;
+        for (size_t k = 0; k < s->blocks.size(); ++k) pt[b * e->pt_stride + k] = s->blocks[k];
+        ReqDev& r = rd[b];
+        memset(&r, 0, sizeof(r));
+        r.philox_seed = s->seed;
+        r.session_id = (uint32_t)s->id;
+        r.round_id = q.round_id;
+        r.ctx = s->len;
+        for (int j = 0; j < gamma; ++j) r.drafts[j] = q.draft_tokens[j];
+        if (q.draft_probs) {
+            if (q.probs_on_host) {
+                if (!e->probs_stage)
+                    CK(cudaMalloc(&e->probs_stage, (size_t)e->opts.max_batch * e->opts.max_gamma * e->V * 4));
+                float* dst = e->probs_stage + (size_t)b * e->opts.max_gamma * e->V;
+                CK(cudaMemcpyAsync(dst, q.draft_probs, (size_t)gamma * e->V * 4, cudaMemcpyHostToDevice, st));
+                r.probs = (uint64_t)dst;
+            } else {
+                r.probs = (uint64_t)q.draft_probs;
+            }
+        }
+        max_len = std::max(max_len, s->len + G);
+        s->busy = true;
+    }
+    t->nb = nb;
+    t->gamma = gamma;
+    t->seq = ++e->seq;
+    *(uint64_t*)(mh + e->off_seq) = t->seq;
+    t->has_gpu = nb > 0;
+    CK(cudaEventCreateWithFlags(&t->ev_done, cudaEventDisableTiming));
+    if (t->has_gpu) {
+        int nchunk = (max_len + 63) / 64;
+        nchunk = std::min(e->max_nchunk, (nchunk + 3) / 4 * 4);
+        sv_status s = run_step(e, st, nb, gamma, exit_layer, nchunk);
+        if (s) {
+            e->poisoned = true;
+            for (auto* ss : t->sess) ss->busy = false;
+            delete t;
+            return s;
+        }
+    }
+    CK(cudaEventRecord(t->ev_done, st));
+    e->inflight = t;
+    *out = t;
+    return SV_OK;
+}
+
+static void fill_host_result(sv_exit_result* r, const sv_ticket* t, int i, int exit_layer, int is_final) {
+    memset(r, 0, sizeof(*r));
+    r->round_id = t->rounds[i];
+    r->exit_layer = exit_layer;
+    r->is_final = is_final;
+    r->status = t->host_status[i];
+    r->new_len = t->ctx[i];
+    for (int k = 0; k <= SV_MAX_GAMMA; ++k) r->tokens[k] = -1;
+}
+
+extern "C" sv_status sv_wait_early(sv_ticket* t, int64_t timeout_us) {
+    if (!t) return fail(SV_E_INVALID, "NULL ticket");
+    sv_engine* e = t->e;
+    if (t->exit_layer == 0 || t->early_done) return SV_OK;
+    if (t->has_gpu) {
+        const auto t0 = std::chrono::steady_clock::now();
+        while (*e->mb_flag != t->seq) {
+            if (cudaEventQuery(t->ev_done) == cudaSuccess) break;   // step already complete
+            if (timeout_us >= 0 &&
+                std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count() >
+                    timeout_us)
+                return fail(SV_E_TIMEOUT, "early result not ready");
+            std::this_thread::yield();
+        }
+    }
+    for (int i = 0; i < t->n; ++i) {
+        if (t->gpu_slot[i] >= 0) t->early[i] = e->mb_exit[t->gpu_slot[i]];
+        else fill_host_result(&t->early[i], t, i, t->exit_layer, 0);
+    }
+    t->early_done = true;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us) {
+    if (!t) return fail(SV_E_INVALID, "NULL ticket");
+    sv_engine* e = t->e;
+    if (t->final_done) return SV_OK;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        cudaError_t q = cudaEventQuery(t->ev_done);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) {
+            e->poisoned = true;
+            return fail(SV_E_DEVICE, std::string("step failed: ") + cudaGetErrorString(q));
+        }
+        if (timeout_us >= 0 &&
+            std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count() >
+                timeout_us)
+            return fail(SV_E_TIMEOUT, "final result not ready");
+        std::this_thread::yield();
+    }
+    if (t->exit_layer > 0 && !t->early_done) sv_wait_early(t, -1);
+    std::lock_guard<std::mutex> lk(e->mu);
+    for (int i = 0; i < t->n; ++i) {
+        sv_session* s = t->sess[i];
+        if (t->gpu_slot[i] >= 0) {
+            t->final_[i] = e->mb_final[t->gpu_slot[i]];
+            const sv_exit_result& r = t->final_[i];
+            if (r.status == SV_OK) {   // S14: rollback = keep ctx + 1 + delta rows
+                s->len = r.new_len;
+                s->last_round = r.round_id;
+            }
+            s->busy = false;
+        } else {
+            fill_host_result(&t->final_[i], t, i, e->L, 1);
+        }
+    }
+    t->final_done = true;
+    e->inflight = nullptr;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_ticket_release(sv_ticket* t) {
+    if (!t) return fail(SV_E_INVALID, "NULL ticket");
+    if (!t->final_done) {
+        sv_status s = sv_wait_final(t, -1);
+        if (s) return s;
+    }
+    cudaEventDestroy(t->ev_done);
+    delete t;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_verify(sv_session* s, const sv_verify_req* req, int32_t exit_layer, sv_exit_result* early,
+                               sv_exit_result* final_) {
+    if (!s || !req) return fail(SV_E_INVALID, "NULL argument");
+    if (req->session != s) return fail(SV_E_INVALID, "request session mismatch");
+    sv_ticket* t = nullptr;
+    sv_status st = sv_verify_submit(s->e, req, 1, exit_layer, early, final_, nullptr, &t);
+    if (st) return st;
+    if ((st = sv_wait_early(t, -1))) return st;
+    if ((st = sv_wait_final(t, -1))) return st;
+    return sv_ticket_release(t);
+}
+
+// ------------------------------------------------------------------ test hooks
+extern "C" sv_status sv_debug_logits(sv_ticket* t, int32_t which, float* dst) {
+    if (!t || !dst || (which != 0 && which != 1)) return fail(SV_E_INVALID, "bad arguments");
+    sv_engine* e = t->e;
+    if (!t->final_done) {
+        sv_status s = sv_wait_final(t, -1);
+        if (s) return s;
+    }
+    if (which == 0 && t->exit_layer == 0) return fail(SV_E_INVALID, "step had no early exit");
+    if (!t->has_gpu) return SV_OK;
+    const size_t bytes = (size_t)t->nb * (t->gamma + 1) * e->V * 4;
+    CK(cudaMemcpy(dst, which == 0 ? e->logits_exit : e->logits_final, bytes, cudaMemcpyDeviceToDevice));
+    return SV_OK;
+}
+
+extern "C" sv_status sv_debug_accept(sv_engine* e, const float* logits_dev, const sv_verify_req* reqs, int32_t n,
+                                     sv_exit_result* out) {
+    if (!e || !logits_dev || !reqs || !out || n < 1 || n > e->opts.max_batch) return fail(SV_E_INVALID, "bad arguments");
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (e->inflight) return fail(SV_E_BUSY, "a ticket is in flight");
+    const int gamma = reqs[0].gamma;
+    if (gamma < 1 || gamma > e->opts.max_gamma) return fail(SV_E_INVALID, "gamma out of range");
+    CK(cudaSetDevice(e->device));
+    ReqDev* rd = (ReqDev*)(e->meta_host + e->off_reqdev);
+    for (int i = 0; i < n; ++i) {
+        const sv_verify_req& q = reqs[i];
+        if (!q.session || q.gamma != gamma || !q.draft_tokens) return fail(SV_E_INVALID, "bad request");
+        ReqDev& r = rd[i];
+        memset(&r, 0, sizeof(r));
+        r.philox_seed = q.session->seed;
+        r.session_id = (uint32_t)q.session->id;
+        r.round_id = q.round_id;
+        r.ctx = q.session->len;
+        for (int j = 0; j < gamma; ++j) {
+            if (q.draft_tokens[j] < 0 || q.draft_tokens[j] >= e->V) return fail(SV_E_INVALID, "draft token range");
+            r.drafts[j] = q.draft_tokens[j];
+        }
+        if (q.draft_probs && q.probs_on_host) return fail(SV_E_INVALID, "debug_accept takes device probs");
+        r.probs = (uint64_t)q.draft_probs;
+    }
+    CK(cudaMemcpy(e->meta_dev + e->off_reqdev, rd, (size_t)n * sizeof(ReqDev), cudaMemcpyHostToDevice));
+    AcceptArgs aa = {};
+    aa.logits = logits_dev;
+    aa.req = (const ReqDev*)(e->meta_dev + e->off_reqdev);
+    aa.stats = e->stats_final;
+    aa.race = e->race_final;
+    aa.counters = e->cnt_acc_final;
+    aa.out = e->res_final_dev;
+    aa.B = n; aa.G = gamma + 1; aa.V = e->V; aa.nch = e->acc_nch; aa.chunk = e->acc_chunk;
+    aa.exit_layer = e->L; aa.is_final = 1;
+    CK(accept_launch(aa, 0));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out, e->res_final_dev, (size_t)n * sizeof(sv_exit_result), cudaMemcpyDeviceToHost));
+    return SV_OK;
+}
+
+extern "C" sv_status sv_debug_kv_rows(sv_session* s, int32_t layer, int32_t first, int32_t count, void* k_host,
+                                      void* v_host) {
+    if (!s || !k_host || !v_host) return fail(SV_E_INVALID, "NULL argument");
+    sv_engine* e = s->e;
+    const int P = e->cfg.page_tokens, D = e->D, H = e->H;
+    if (layer < 0 || layer >= e->L || first < 0 || count < 0 ||
+        (size_t)(first + count) > s->blocks.size() * (size_t)P)
+        return fail(SV_E_INVALID, "rows out of range");
+    CK(cudaSetDevice(e->device));
+    CK(cudaDeviceSynchronize());
+    for (int i = 0; i < count; ++i) {
+        const int pos = first + i;
+        const size_t blk = s->blocks[pos / P];
+        for (int kv = 0; kv < 2; ++kv) {
+            const uint8_t* src = e->kv_pool + blk * e->blk_bytes +
+                                 (((size_t)layer * 2 + kv) * H * P + (size_t)(pos % P)) * D * 2;
+            uint8_t* dst = (uint8_t*)(kv ? v_host : k_host) + (size_t)i * e->d * 2;
+            CK(cudaMemcpy2D(dst, (size_t)D * 2, src, (size_t)P * D * 2, (size_t)D * 2, H, cudaMemcpyDeviceToHost));
+        }
+    }
+    return SV_OK;
+}
+
+extern "C" sv_status sv_debug_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    if (!ctr || !key || !out) return fail(SV_E_INVALID, "NULL argument");
+    sv_status s = require_sm100(0);
+    if (s) {
+        int dev = -1;
+        if (cudaGetDevice(&dev) != cudaSuccess || require_sm100(dev)) return s;
+    }
+    uint32_t* d = nullptr;
+    uint32_t in[6] = {ctr[0], ctr[1], ctr[2], ctr[3], key[0], key[1]};
+    CK(cudaMalloc(&d, 64));
+    CK(cudaMemcpy(d, in, 24, cudaMemcpyHostToDevice));
+    CK(philox_launch(d, d + 8, 0));
+    CK(cudaMemcpy(out, d + 8, 16, cudaMemcpyDeviceToHost));
+    CK(cudaFree(d));
+    return SV_OK;
+}

@@ -1,0 +1,378 @@
+// gemm.cu — K1: bf16 weight-streaming GEMM on 5th-generation tensor cores.
+//
+//   out[m, n] = sum_k X[m, k] * W[n, k]      (X: activations [M, K], W: weights [N, K])
+//
+// computed "swap-AB": the weight tile is the MMA A operand (M_mma = 128 weight
+// rows = 128 output features) and the token block is the B operand
+// (N_mma = TILE_N tokens, 16..256), so a batch-1 verify step (gamma+1 = 5 query
+// rows) still fills the 128-row MMA and every weight byte is read exactly once.
+//
+// Per CTA: one 128-row weight tile x one TILE_N token tile x one K split.
+//   warp 0 / lane 0 : TMA producer (weights evict-first, activations evict-last),
+//                     STAGES-deep mbarrier ring of 64-wide K blocks (128 B rows,
+//                     128B swizzle); weight loads are issued BEFORE
+//                     griddepcontrol.wait so they overlap the previous kernel.
+//   warp 1 / lane 0 : tcgen05.mma.cta_group::1.kind::f16 issuer, fp32 accumulator
+//                     in TMEM (TILE_N columns), tcgen05.commit frees smem slots.
+//   all 4 warps     : epilogue, TMEM -> registers (tcgen05.ld 32x32b) -> smem tile
+//                     -> fused op, or -> split-K partials; the last CTA of a tile
+//                     (atomic ticket) reduces the partials in split order 0..S-1,
+//                     so results are deterministic and independent of the other
+//                     token columns (row invariance used by the rollback pin).
+//
+// Fused epilogues:
+//   EPI_QKV    : y = acc * rstd[m]; RoPE (rotate-half, table cos/sin) on q and k;
+//                q -> fp32 buffer, k and v -> paged KV cache at pos[m]   (Eq. 3)
+//   EPI_RESID  : h += acc (fp32 residual); u = bf16(h * g_next) for the next
+//                RMSNorm; sum(h^2) per 128-column tile -> ssq partials
+//   EPI_SWIGLU : act = bf16(silu(gate * rstd) * (up * rstd))
+//   EPI_LOGITS : z = acc * rstd[m] (fp32 logits, LM head)
+// RMSNorm is folded: the GEMM consumes u = bf16(h * g) and multiplies its
+// accumulator by rstd[m] = 1/sqrt(sum(h^2)/d + eps) from the producer's partials.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sv {
+
+constexpr int BK = 64;                      // K elements per stage (one 128 B swizzle row)
+constexpr int TM = 128;                     // weight rows per tile (UMMA M)
+constexpr int A_STAGE = TM * BK * 2;        // 16 KB
+constexpr int EPI_CHUNK = 16;               // token columns per epilogue pass
+
+template <int TN>
+struct GemmCfg {
+    static constexpr int B_STAGE = TN * BK * 2;
+    static constexpr int STAGE = A_STAGE + B_STAGE;
+    // small token tiles: 2 CTAs per SM (<= 113 KB each), else 1 CTA per SM
+    static constexpr int BUDGET = (TN <= 64 ? 113 * 1024 : 225 * 1024) - 1024 - 4096;
+    static constexpr int STAGES_RAW = BUDGET / STAGE;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+    static constexpr int TMEM_COLS = TN < 32 ? 32 : TN;
+    static constexpr int AUX = 4096;        // barriers, tmem slot, rstd[TN], reductions
+    static constexpr int SMEM = 1024 + STAGES * STAGE + AUX;
+    static_assert(STAGES >= 2, "pipeline too shallow");
+    static_assert(EPI_CHUNK * TM * 4 <= STAGES * STAGE, "epilogue tile must fit the ring");
+};
+
+template <int EPI>
+__device__ __forceinline__ void epi_chunk(const GemmArgs& a, const float* sOut, const float* sR, float* sRed,
+                                          int tok0, int m0, int n0, int nt) {
+    const int r = threadIdx.x;
+    const int warp = r >> 5, lane = r & 31;
+    if constexpr (EPI == EPI_QKV) {
+        const int d = a.d_model, D = a.head_dim, half = D >> 1;
+        const int sec = n0 / d;                // 0 = q, 1 = k, 2 = v
+        const int col = (n0 % d) + r;
+        const int hd = col / D, i = col % D;
+        const int rp = r - i + ((i + half) % D);
+        for (int j = 0; j < EPI_CHUNK; ++j) {
+            const int tok = tok0 + j;
+            if (tok >= a.M) break;
+            const float rs = sR[tok - m0];
+            float v = sOut[j * TM + r] * rs;
+            const int pos = a.meta.pos[tok];
+            if (sec < 2) {
+                const float vp = sOut[j * TM + rp] * rs;
+                const float2 cs = reinterpret_cast<const float2*>(a.rope_cs)[(size_t)pos * half + (i % half)];
+                v = (i < half) ? (v * cs.x - vp * cs.y) : (v * cs.x + vp * cs.y);
+            }
+            if (sec == 0) {
+                a.qbuf[(size_t)tok * d + col] = v;
+            } else {
+                const int b = a.meta.row_req[tok];
+                const int blk = a.meta.page_table[b * a.meta.pt_stride + pos / a.page_tokens];
+                const int slot = pos % a.page_tokens;
+                const size_t off = (((size_t)blk * a.n_layers + a.layer) * 2 + (sec - 1)) *
+                                       ((size_t)a.n_heads * a.page_tokens * D) +
+                                   ((size_t)hd * a.page_tokens + slot) * D + i;
+                reinterpret_cast<bf16*>(a.kv_pool)[off] = __float2bfloat16_rn(v);
+            }
+        }
+    } else if constexpr (EPI == EPI_RESID) {
+        const int d = a.d_model;
+        const float g = __bfloat162float(reinterpret_cast<const bf16*>(a.g_out)[n0 + r]);
+        const float g2 = a.u_out2 ? __bfloat162float(reinterpret_cast<const bf16*>(a.g_out2)[n0 + r]) : 0.f;
+        for (int j = 0; j < EPI_CHUNK; ++j) {
+            const int tok = tok0 + j;
+            float hv = 0.f;
+            if (tok < a.M) {
+                const size_t idx = (size_t)tok * d + n0 + r;
+                hv = a.h[idx] + sOut[j * TM + r];
+                a.h[idx] = hv;
+                reinterpret_cast<bf16*>(a.u_out)[idx] = __float2bfloat16_rn(hv * g);
+                if (a.u_out2) reinterpret_cast<bf16*>(a.u_out2)[idx] = __float2bfloat16_rn(hv * g2);
+            }
+            const float sq = warp_sum(hv * hv);
+            if (lane == 0) sRed[warp * EPI_CHUNK + j] = sq;
+        }
+        __syncthreads();
+        if (r < EPI_CHUNK && tok0 + r < a.M) {
+            const float s = (sRed[0 * EPI_CHUNK + r] + sRed[1 * EPI_CHUNK + r]) +
+                            (sRed[2 * EPI_CHUNK + r] + sRed[3 * EPI_CHUNK + r]);
+            a.ssq_out[(size_t)nt * a.MP + tok0 + r] = s;
+        }
+    } else if constexpr (EPI == EPI_SWIGLU) {
+        const int rr = r & 63, jh = r >> 6;
+        for (int j = jh * (EPI_CHUNK / 2); j < (jh + 1) * (EPI_CHUNK / 2); ++j) {
+            const int tok = tok0 + j;
+            if (tok >= a.M) break;
+            const float rs = sR[tok - m0];
+            const float g = sOut[j * TM + rr] * rs;
+            const float u = sOut[j * TM + 64 + rr] * rs;
+            const float y = g / (1.0f + expf(-g)) * u;
+            reinterpret_cast<bf16*>(a.act)[(size_t)tok * a.d_ff + nt * 64 + rr] = __float2bfloat16_rn(y);
+        }
+    } else {  // EPI_LOGITS
+        for (int j = 0; j < EPI_CHUNK; ++j) {
+            const int tok = tok0 + j;
+            if (tok >= a.M) break;
+            a.logits[(size_t)tok * a.N + n0 + r] = sOut[j * TM + r] * sR[tok - m0];
+        }
+    }
+}
+
+template <int TN, int EPI>
+__global__ void __launch_bounds__(128, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ GemmArgs a) {
+    using C = GemmCfg<TN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + C::STAGES * A_STAGE;
+    uint8_t* aux = smem + C::STAGES * C::STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(aux);
+    uint64_t* empty = full + C::STAGES;
+    uint64_t* done = empty + C::STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
+    float* sR = reinterpret_cast<float*>(aux + 256);          // [TN]
+    float* sRed = sR + 256;                                   // [4][EPI_CHUNK]
+    float* sOut = reinterpret_cast<float*>(smem);             // [EPI_CHUNK][128], reuses the ring
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nt = blockIdx.x, mt = blockIdx.y, split = blockIdx.z;
+    const int NT = gridDim.x, MT = gridDim.y;
+    const int n0 = nt * TM, m0 = mt * TN;
+    const int KB = a.K / BK;
+    const int kb0 = (int)((long long)KB * split / a.splits);
+    const int kb1 = (int)((long long)KB * (split + 1) / a.splits);
+    const int nk = kb1 - kb0;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer
+        const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+        const int pre = nk < C::STAGES ? nk : C::STAGES;
+        for (int i = 0; i < pre; ++i) {   // weights do not depend on the previous kernel
+            mbar_arrive_expect_tx(&full[i], C::STAGE);
+            tma_load_2d(&tmA, sA + i * A_STAGE, &full[i], (kb0 + i) * BK, n0, pol_w);
+        }
+        pdl_wait();
+        for (int i = 0; i < pre; ++i) tma_load_2d(&tmB, sB + i * C::B_STAGE, &full[i], (kb0 + i) * BK, m0, pol_x);
+        for (int i = pre; i < nk; ++i) {
+            const int s = i % C::STAGES;
+            mbar_wait(&empty[s], ((i / C::STAGES) - 1) & 1);
+            mbar_arrive_expect_tx(&full[s], C::STAGE);
+            tma_load_2d(&tmA, sA + s * A_STAGE, &full[s], (kb0 + i) * BK, n0, pol_w);
+            tma_load_2d(&tmB, sB + s * C::B_STAGE, &full[s], (kb0 + i) * BK, m0, pol_x);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer (single thread)
+        constexpr uint32_t idesc = umma_idesc_bf16(TM, TN);
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % C::STAGES;
+            mbar_wait(&full[s], (i / C::STAGES) & 1);
+            tc_fence_after();
+            const uint64_t ad = umma_sdesc_sw128(smem_u32(sA + s * A_STAGE));
+            const uint64_t bd = umma_sdesc_sw128(smem_u32(sB + s * C::B_STAGE));
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)   // +32 B per K=16 step inside the swizzle atom
+                umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) ? 1u : 0u);
+            umma_commit(&empty[s]);
+        }
+        umma_commit(done);
+    }
+    __syncwarp();
+    pdl_wait();   // everything below reads data produced by the previous kernel
+
+    // rstd of the RMSNorm folded into this GEMM (fixed summation order)
+    for (int t = threadIdx.x; t < TN; t += blockDim.x) {
+        const int tok = m0 + t;
+        float rs = 1.0f;
+        if (a.ssq_in && tok < a.M) {
+            float s = 0.f;
+            for (int k = 0; k < a.ssq_tiles; ++k) s += a.ssq_in[(size_t)k * a.MP + tok];
+            rs = 1.0f / sqrtf(s * a.inv_d + a.eps);
+        }
+        sR[t] = rs;
+    }
+
+    mbar_wait(done, 0);
+    tc_fence_after();
+    pdl_launch_dependents();
+
+    const int row = warp * 32 + lane;
+    const uint32_t tbase = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const bool direct = (a.splits == 1);
+    for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
+        if (m0 + c0 >= a.M) break;                       // CTA-uniform
+        uint32_t r[16];
+        tmem_ld_32x32b_x16(tbase + c0, r);
+        tmem_ld_wait();
+        if (direct) {
+            __syncthreads();                             // sR visible / previous chunk consumed
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sOut[j * TM + row] = __uint_as_float(r[j]);
+            __syncthreads();
+            epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt);
+        } else {
+            float* wsp = a.ws + (((size_t)split * NT + nt) * a.MP) * TM;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int tok = m0 + c0 + j;
+                if (tok < a.M) wsp[(size_t)tok * TM + row] = __uint_as_float(r[j]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
+    if (direct) return;
+
+    // ---------------- split-K: the last CTA of this tile reduces in split order
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int old = atomicAdd(&a.counters[nt * MT + mt], 1);
+        *s_flag = (old == a.splits - 1);
+    }
+    __syncthreads();
+    if (!*s_flag) return;
+    __threadfence();
+    for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
+        if (m0 + c0 >= a.M) break;
+        for (int j = 0; j < EPI_CHUNK; ++j) {
+            const int tok = m0 + c0 + j;
+            float acc = 0.f;
+            if (tok < a.M)
+                for (int s = 0; s < a.splits; ++s)
+                    acc += __ldcg(&a.ws[(((size_t)s * NT + nt) * a.MP + tok) * TM + row]);
+            sOut[j * TM + row] = acc;
+        }
+        __syncthreads();
+        epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a.counters[nt * MT + mt] = 0;
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows) {
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t gdim[2] = {K, rows};
+    cuuint64_t gstride[1] = {K * 2};
+    cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box,
+                          estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+int gemm_pick_tile_n(int M) {
+    if (M <= 16) return 16;
+    if (M <= 32) return 32;
+    if (M <= 64) return 64;
+    if (M <= 128) return 128;
+    return 256;
+}
+
+int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms) {
+    const int ntiles = (N / TM) * ((M + tile_n - 1) / tile_n);
+    const int per_sm = tile_n <= 64 ? 2 : 1;
+    const int slots = num_sms * per_sm;
+    const int KB = K / BK;
+    int s = slots / ntiles;
+    if (s < 1) s = 1;
+    if (s > KB / 2) s = KB / 2 > 0 ? KB / 2 : 1;   // >= 2 K blocks per split
+    return s;
+}
+
+template <int TN, int EPI>
+static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, cudaStream_t st) {
+    using C = GemmCfg<TN>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_kernel<TN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.N / TM, (a.M + TN - 1) / TN, a.splits);
+    cfg.blockDim = dim3(128, 1, 1);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<TN, EPI>, tmA, tmB, a);
+}
+
+template <int TN>
+static cudaError_t launch_epi(int epi, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
+                              cudaStream_t st) {
+    switch (epi) {
+        case EPI_QKV: return launch_t<TN, EPI_QKV>(tmA, tmB, a, st);
+        case EPI_RESID: return launch_t<TN, EPI_RESID>(tmA, tmB, a, st);
+        case EPI_SWIGLU: return launch_t<TN, EPI_SWIGLU>(tmA, tmB, a, st);
+        case EPI_LOGITS: return launch_t<TN, EPI_LOGITS>(tmA, tmB, a, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t gemm_launch(int epi, int tile_n, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
+                        cudaStream_t st) {
+    switch (tile_n) {
+        case 16: return launch_epi<16>(epi, tmA, tmB, a, st);
+        case 32: return launch_epi<32>(epi, tmA, tmB, a, st);
+        case 64: return launch_epi<64>(epi, tmA, tmB, a, st);
+        case 128: return launch_epi<128>(epi, tmA, tmB, a, st);
+        case 256: return launch_epi<256>(epi, tmA, tmB, a, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace sv

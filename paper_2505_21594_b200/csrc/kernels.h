@@ -1,0 +1,131 @@
+// kernels.h — host-side launch interface of the verify-step kernels (internal).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sv.h"
+
+namespace sv {
+
+typedef uint16_t bf16_raw_t;   // raw bf16 storage in host-visible structs
+
+// ----------------------------------------------------------------- GEMM (K1)
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_LOGITS = 3 };
+
+// Per-step request metadata, device resident (one H2D per step).
+struct StepMeta {
+    int32_t* tok;         // [rows] token id of each query row
+    int32_t* pos;         // [rows] absolute position
+    int32_t* ctx;         // [B] cached length before the step
+    int32_t* row_req;     // [rows] request index of each query row
+    int32_t* page_table;  // [B][pt_stride] KV block ids
+    int32_t pt_stride;
+};
+
+struct GemmArgs {
+    // problem: out[M, N] = B[M, K] . A[N, K]^T  (A = weights, B = activations)
+    int N, K, M, MP;     // MP = padded rows of the activation buffer
+    int splits;          // split-K factor (deterministic reduction, fixed order)
+    float* ws;           // split-K partials [splits][ntiles][MP][128]
+    int* counters;       // [ntiles * mtiles], zero on entry, reset by the reducer
+    // RMSNorm folding: rstd[m] = 1/sqrt(sum_t ssq_in[t][m] / d + eps)
+    const float* ssq_in;  // [ssq_tiles][MP] or nullptr (no scaling)
+    int ssq_tiles;
+    float inv_d, eps;
+    // EPI_QKV
+    float* qbuf;          // [MP][d] fp32 (RoPE applied)
+    bf16_raw_t* kv_pool;  // KV pool base (bf16)
+    StepMeta meta;
+    int layer, n_layers, n_heads, head_dim, d_model, page_tokens;
+    const float* rope_cs;  // [max_pos][head_dim/2][2] (cos, sin) fp32
+    // EPI_RESID
+    float* h;             // [MP][d] fp32 residual stream (in/out)
+    const void* g_out;    // bf16 [d] gain of the next RMSNorm
+    void* u_out;          // bf16 [MP][d] = h * g_out
+    const void* g_out2;   // bf16 [d] or nullptr (early-exit copy with the final gain)
+    void* u_out2;
+    float* ssq_out;       // [d/128][MP] per-tile sum of h^2
+    // EPI_SWIGLU
+    void* act;            // bf16 [MP][d_ff]
+    int d_ff;
+    // EPI_LOGITS
+    float* logits;        // [M][N]
+};
+
+// Encodes a 2D bf16 K-major tensor map (rows x K), box = 64 x box_rows, SW128.
+bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows);
+
+int gemm_pick_tile_n(int M);
+int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms);
+cudaError_t gemm_launch(int epi, int tile_n, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
+                        cudaStream_t st);
+
+// ------------------------------------------------------------- attention (K3)
+struct AttnArgs {
+    const float* q;       // [MP][d]
+    const bf16_raw_t* kv_pool;
+    void* out;            // bf16 [MP][d]
+    float* part_o;        // [B*H][nchunk][G][head_dim]
+    float* part_ml;       // [B*H][nchunk][G][2]
+    int* counters;        // [B*H]
+    const int32_t* ctx;   // [B]
+    const int32_t* page_table;
+    int pt_stride;
+    int B, G, n_heads, head_dim, d_model, n_layers, layer, page_tokens, nchunk;
+    float scale_log2;     // log2(e) / sqrt(head_dim)
+};
+cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st);
+
+// ----------------------------------------------------------- acceptance (K5)
+struct ReqDev {            // per-request metadata for the acceptance kernels
+    uint64_t probs;        // device pointer to q [gamma][V] or 0 (greedy)
+    uint64_t philox_seed;
+    uint32_t session_id;
+    uint32_t round_id;
+    int32_t ctx;
+    int32_t status_in;     // host-detected status (nonzero: skip)
+    int32_t drafts[SV_MAX_GAMMA];
+};
+struct RowStat {
+    float m1, m2, sum;
+    int32_t idx;
+};
+struct RacePart {
+    float k1, k2, f1;
+    int32_t v1, fv1;
+    int32_t pad[3];
+};
+struct AcceptArgs {
+    const float* logits;    // [B*G][V]
+    const ReqDev* req;      // [B]
+    RowStat* stats;         // [B*G][nch]
+    RacePart* race;         // [B][nch]
+    int* counters;          // [B]
+    sv_exit_result* out;    // [B] device
+    int B, G, V, nch, chunk;
+    int exit_layer, is_final;
+};
+cudaError_t accept_launch(const AcceptArgs& a, cudaStream_t st);
+int accept_chunks(int V, int* chunk);
+
+// ------------------------------------------------------------- misc (K4 K7 K8)
+struct EmbedArgs {
+    const int32_t* tok;
+    const void* embed;   // bf16 [V][d]
+    const void* gain;    // bf16 [d]
+    float* h;            // [MP][d]
+    void* u;             // bf16 [MP][d]
+    float* ssq;          // [d/128][MP]
+    int M, MP, d;
+};
+cudaError_t embed_launch(const EmbedArgs& a, cudaStream_t st);
+
+enum GenLayout { GEN_PLAIN = 0, GEN_QKV = 1, GEN_GU = 2 };
+cudaError_t gen_launch(void* dst, uint64_t n, int layout, uint64_t seed, uint64_t tid0, int rows_per_sec,
+                       int cols, float c, float offset, cudaStream_t st);
+cudaError_t kvfill_launch(bf16_raw_t* pool, const int32_t* blocks, int nblocks, int len, uint64_t kv_seed,
+                          int n_layers, int n_heads, int head_dim, int page_tokens, float c, cudaStream_t st);
+cudaError_t philox_launch(const uint32_t* ctr_key, uint32_t* out, cudaStream_t st);
+
+}  // namespace sv

@@ -1,0 +1,135 @@
+"""GPU unit parity: Philox, weight / KV generators (bit-exact), acceptance kernels
+on identical fp32 logits (level U of DESIGN.md "Parity contract")."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import accept as oacc
+from oracle import gen
+from workload import drafts as wd
+from workload import tiny
+from workload.configs import ModelCfg
+
+from .gpu_helpers import Tally
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "philox_kat.txt")
+
+
+def test_philox_kat_on_device(svlib):
+    from paper_2505_21594_b200 import sv
+    for line in open(GOLDEN):
+        if line.startswith("#") or not line.strip():
+            continue
+        v = [int(t, 16) for t in line.split()]
+        assert sv.debug_philox(v[:4], v[4:6]) == v[6:]
+
+
+def _bits(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+@pytest.fixture(scope="module")
+def tiny_weights(svlib):
+    from paper_2505_21594_b200 import sv
+    return sv.Weights(tiny(), seed=1)
+
+
+def test_weights_bit_identical_tiny(tiny_weights):
+    mc = tiny()
+    W = tiny_weights
+    d, F, V = mc.d_model, mc.d_ff, mc.vocab
+    sg = gen.sigmas(mc)
+    assert np.array_equal(_bits(W.tensor("embed")), gen.gen_bits(1, gen.TID_EMBED, V * d, sg["embed"]).reshape(V, d))
+    assert np.array_equal(_bits(W.tensor("lm_head")), gen.gen_bits(1, gen.TID_LM_HEAD, V * d, sg["lm_head"]).reshape(V, d))
+    assert np.array_equal(_bits(W.tensor("norm_final")), gen.gen_bits(1, gen.TID_NORM_FINAL, d, 0.1, 1.0))
+    for l in range(mc.n_layers):
+        t = lambda k: gen.layer_tid(l, k)
+        qkv = _bits(W.tensor("qkv", l))
+        for s, k in enumerate((gen.WQ, gen.WK, gen.WV)):
+            assert np.array_equal(qkv[s * d:(s + 1) * d], gen.gen_bits(1, t(k), d * d, sg["w_in"]).reshape(d, d))
+        assert np.array_equal(_bits(W.tensor("o", l)), gen.gen_bits(1, t(gen.WO), d * d, sg["w_out"]).reshape(d, d))
+        gu = _bits(W.tensor("gu", l)).reshape(F // 64, 2, 64, d)      # 64-row interleave
+        wg = gen.gen_bits(1, t(gen.WG), F * d, sg["w_in"]).reshape(F // 64, 64, d)
+        wu = gen.gen_bits(1, t(gen.WU), F * d, sg["w_in"]).reshape(F // 64, 64, d)
+        assert np.array_equal(gu[:, 0], wg) and np.array_equal(gu[:, 1], wu)
+        assert np.array_equal(_bits(W.tensor("down", l)), gen.gen_bits(1, t(gen.WDOWN), d * F, sg["w_out"]).reshape(d, F))
+        assert np.array_equal(_bits(W.tensor("norm_attn", l)), gen.gen_bits(1, t(gen.G_ATTN), d, 0.1, 1.0))
+        assert np.array_equal(_bits(W.tensor("norm_mlp", l)), gen.gen_bits(1, t(gen.G_MLP), d, 0.1, 1.0))
+
+
+def test_kv_fill_bit_identical(svlib, tiny_weights):
+    from paper_2505_21594_b200 import sv
+    mc = tiny()
+    eng = sv.Engine(mc, tiny_weights, max_batch=1, max_gamma=8)
+    s = eng.open_session(1, 4)
+    s.fill_kv(100, kv_seed=2)
+    assert s.length == 100
+    for l in range(mc.n_layers):
+        k, v = s.kv_rows(l, 0, 100)
+        for kv, got in ((0, k), (1, v)):
+            ref = gen.gen_bits(2, gen.kv_tid(l, kv), 100 * mc.d_model, 1.0).reshape(100, mc.d_model)
+            assert np.array_equal(got, ref)
+    s.close()
+    eng.close()
+
+
+def _accept_case(eng, mc, B, gamma, seed, greedy, sessions):
+    from paper_2505_21594_b200 import sv
+    V = mc.vocab
+    logits, x, q = wd.synthetic_accept_case(seed, B, gamma, V)
+    zl = torch.from_numpy(logits).cuda()
+    qd = torch.from_numpy(q).cuda()
+    reqs = []
+    for b in range(B):
+        reqs.append(sv.Request(sessions[b], 1 + seed % 1000, 0, x[b], None if greedy else qd[b]))
+    got = eng.debug_accept(zl, reqs)
+    refs = []
+    for b in range(B):
+        s = sessions[b]
+        refs.append(oacc.accept(logits[b].astype(np.float64), x[b], None if greedy else q[b].astype(np.float64),
+                                seed=s.philox_seed, session_id=s.session_id, round_id=1 + seed % 1000))
+    return refs, got
+
+
+@pytest.mark.parametrize("V", [512, 32000])
+@pytest.mark.parametrize("greedy", [True, False])
+def test_accept_matches_oracle_on_identical_logits(svlib, V, greedy):
+    """Level U: K5 vs oracle on the same fp32 logits / draft probs / counters:
+    delta and tokens bit-exact wherever every decision margin > 1e-3."""
+    from paper_2505_21594_b200 import sv
+    mc = ModelCfg(n_layers=1, d_model=128, n_heads=4, d_ff=128, vocab=V, max_ctx=256)
+    W = sv.Weights(mc, seed=1)
+    eng = sv.Engine(mc, W, max_batch=8, max_gamma=8)
+    sessions = [eng.open_session(100 + b, 0x1234 + 77 * b) for b in range(8)]
+    tally = Tally()
+    for gamma in (1, 2, 4, 8):
+        for seed in range(6):
+            refs, got = _accept_case(eng, mc, 8, gamma, seed * 10 + gamma, greedy, sessions)
+            for r, g in zip(refs, got):
+                tally.add(r, g, 1e-3, tag=(gamma, seed))
+                if r.status == oacc.OK and r.tokens == g.emitted():
+                    assert abs(g.score - r.score) <= 1e-5 * max(1.0, r.score)
+                    assert abs(g.next_prob - r.next_prob) <= 1e-4 * max(1e-3, r.next_prob)
+    print(tally.report())
+    assert not tally.hard_mismatch, tally.hard_mismatch[:3]
+    assert tally.checked >= 0.9 * tally.n
+    for s in sessions:
+        s.close()
+    eng.close()
+
+
+def test_accept_protocol_error_zero_draft_mass(svlib):
+    from paper_2505_21594_b200 import sv
+    mc = ModelCfg(n_layers=1, d_model=128, n_heads=4, d_ff=128, vocab=512, max_ctx=256)
+    eng = sv.Engine(mc, sv.Weights(mc, seed=1), max_batch=2, max_gamma=8)
+    s = eng.open_session(1, 2)
+    logits, x, q = wd.synthetic_accept_case(5, 1, 3, 512)
+    q = q.copy()
+    q[0, 2, x[0, 2]] = 0.0
+    got = eng.debug_accept(torch.from_numpy(logits).cuda(), [sv.Request(s, 1, 0, x[0], torch.from_numpy(q[0]).cuda())])
+    assert got[0].status == sv.SV_E_PROTOCOL
+    s.close()
+    eng.close()

@@ -1,0 +1,226 @@
+"""GPU end-to-end parity of the verify step against the oracle (level E of
+DESIGN.md "Parity contract"): logits within 2e-2 row-max-relative (north star),
+decisions identical wherever the oracle's margin exceeds the propagated bound,
+KV rollback bit-exact, exit side-effect free, protocol errors."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import accept as oacc
+from oracle import gen
+from oracle import model as om
+from oracle.verify import verify_step
+from workload import drafts as wd
+from workload import tiny
+from workload.configs import ModelCfg
+
+from .gpu_helpers import Tally, decision_bound, oracle_session, row_rel_err
+
+pytestmark = pytest.mark.gpu
+LOGIT_TOL = 2e-2
+
+
+def _setup(mc, B, max_gamma=8, use_graphs=True):
+    from paper_2505_21594_b200 import sv
+    W = sv.Weights(mc, seed=1)
+    eng = sv.Engine(mc, W, max_batch=B, max_gamma=max_gamma, use_graphs=use_graphs)
+    return sv, W, eng
+
+
+def _run_rounds(mc, B, gamma, ctx, exit_layer, greedy, rounds, use_graphs=True, model=None):
+    """Run `rounds` verify steps on B sessions through libsv and the oracle in
+    lockstep (each side keeps its own cache); returns the tally and errors."""
+    sv, W, eng = _setup(mc, B, use_graphs=use_graphs)
+    model = model or om.Model(mc, seed=1)
+    gs, os_ = [], []
+    for b in range(B):
+        s = eng.open_session(10 + b, 1000 + b)
+        s.fill_kv(ctx, kv_seed=2 + b)
+        gs.append(s)
+        os_.append(oracle_session(mc, model, 10 + b, 1000 + b, 2 + b, ctx))
+    pending = list(wd.prefix_tokens(3, B, mc.vocab))
+    tally_f, tally_e = Tally(), Tally()
+    errs = []
+    for rnd in range(1, rounds + 1):
+        x, q = wd.timing_drafts(100 + rnd, B, gamma, mc.vocab, s=1.1)
+        qd = torch.from_numpy(q).cuda()
+        reqs = [sv.Request(gs[b], rnd, pending[b], x[b], None if greedy else qd[b]) for b in range(B)]
+        t = eng.submit(reqs, exit_layer=exit_layer)
+        early = t.wait_early() if exit_layer else None
+        final = t.wait_final()
+        zf = t.logits(1, gamma).cpu().numpy()
+        ze = t.logits(0, gamma).cpu().numpy() if exit_layer else None
+        t.release()
+        for b in range(B):
+            out = verify_step(model, os_[b], rnd, pending[b], x[b], None if greedy else q[b].astype(np.float64),
+                              exit_layer=exit_layer)
+            rel, eps = row_rel_err(zf[b], out.final_logits)
+            errs.append(rel.max())
+            tally_f.add(out.final, final[b], decision_bound(eps.max()), tag=("final", rnd, b))
+            if exit_layer:
+                rel_e, eps_e = row_rel_err(ze[b], out.exit_logits)
+                errs.append(rel_e.max())
+                tally_e.add(out.early, early[b], decision_bound(eps_e.max()), tag=("exit", rnd, b))
+            assert gs[b].length == final[b].new_len
+            if out.final.status == oacc.OK and out.final.tokens == final[b].emitted():
+                assert final[b].new_len == out.new_len
+                pending[b] = final[b].emitted()[-1]
+            else:
+                pending[b] = None       # the two sides diverged (counted above): stop
+        if any(p is None for p in pending):
+            break
+    for s in gs:
+        s.close()
+    eng.close()
+    return tally_f, tally_e, np.array(errs)
+
+
+@pytest.mark.parametrize("greedy", [True, False], ids=["greedy", "stochastic"])
+@pytest.mark.parametrize("ctx", [64, 59])
+def test_tiny_end_to_end(svlib, greedy, ctx):
+    """configs[0]: 2 layers, d=128, 4 heads, V=512, ctx 64 (or 59 = 64 - G), gamma=4,
+    batch 1, early exit at layer 1."""
+    tf, te, errs = _run_rounds(tiny(), 1, 4, ctx, 1, greedy, rounds=4)
+    print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
+    assert errs.max() < LOGIT_TOL
+    assert not tf.hard_mismatch and not te.hard_mismatch
+
+
+@pytest.mark.parametrize("gamma", [1, 3, 8])
+def test_tiny_batched_gamma_sweep(svlib, gamma):
+    tf, te, errs = _run_rounds(tiny(), 5, gamma, 37, 2, False, rounds=2)
+    print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
+    assert errs.max() < LOGIT_TOL
+    assert not tf.hard_mismatch and not te.hard_mismatch
+
+
+def test_tiny_no_graphs_matches_graphs(svlib):
+    """Graph replay and direct launches produce bitwise-identical results."""
+    mc = tiny()
+    res = []
+    for ug in (True, False):
+        sv, W, eng = _setup(mc, 2, use_graphs=ug)
+        ss = [eng.open_session(1 + b, 7 + b) for b in range(2)]
+        for b, s in enumerate(ss):
+            s.fill_kv(40, kv_seed=5 + b)
+        x, q = wd.timing_drafts(9, 2, 4, mc.vocab, s=1.1)
+        qd = torch.from_numpy(q).cuda()
+        t = eng.submit([sv.Request(ss[b], 1, 3, x[b], qd[b]) for b in range(2)], exit_layer=1)
+        t.wait_early()
+        f = t.wait_final()
+        res.append(([r.asdict() for r in f], t.logits(1, 4).cpu().numpy()))
+        t.release()
+        eng.close()
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1])
+
+
+def test_exit_is_side_effect_free(svlib):
+    """PAPER.md:177 'all tokens are verified at the final exit': final logits and
+    results are bitwise identical with the early exit on (any layer) or off."""
+    mc = tiny()
+    sv, W, eng = _setup(mc, 1)
+    outs = []
+    for exit_layer in (0, 1, 2):
+        s = eng.open_session(1, 9)
+        s.fill_kv(50, kv_seed=3)
+        x, q = wd.timing_drafts(4, 1, 4, mc.vocab, s=1.1)
+        t = eng.submit([sv.Request(s, 1, 5, x[0], torch.from_numpy(q[0]).cuda())], exit_layer=exit_layer)
+        e = t.wait_early() if exit_layer else None
+        f = t.wait_final()
+        outs.append((f[0].asdict(), t.logits(1, 4).cpu().numpy(), e))
+        t.release()
+        s.close()
+    assert outs[0][0] == outs[1][0] == outs[2][0]
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][1], outs[2][1])
+    # exit at the last layer == final (north star pin), bitwise
+    e2 = outs[2][2][0].asdict()
+    f2 = outs[2][0]
+    for k in ("accepted", "tokens", "score", "next_prob", "status"):
+        assert e2[k] == f2[k], k
+    eng.close()
+
+
+def test_rollback_bit_exact(svlib):
+    """DESIGN.md R22: (i) rows [0, ctx) byte-identical across a step; (ii) two steps
+    that differ only in the rejected suffix leave byte-identical visible caches and
+    byte-identical next steps; (iv) length == ctx + 1 + delta."""
+    mc = tiny()
+    sv, W, eng = _setup(mc, 1)
+    model = om.Model(mc, seed=1)
+    ctx = 30
+    # the target's greedy continuation from the oracle (an input, not a GPU value)
+    osess = oracle_session(mc, model, 1, 1, 4, ctx)
+    c = osess.cache.copy()
+    z, _, _ = om.forward(model, c, [7])
+    a1 = int(np.argmax(z[0]))
+    final_states = []
+    for suffix in ([3, 3, 3], [9, 100, 200]):
+        s = eng.open_session(1, 1)
+        s.fill_kv(ctx, kv_seed=4)
+        k0, v0 = s.kv_rows(0, 0, ctx)
+        drafts = [a1] + [(a1 + 1 + suffix[0]) % mc.vocab] + suffix[1:]
+        _, f = eng.verify([sv.Request(s, 1, 7, drafts)], exit_layer=0)
+        assert f[0].accepted == 1 and s.length == ctx + 1 + 1
+        k1, v1 = s.kv_rows(0, 0, ctx)
+        assert np.array_equal(k0, k1) and np.array_equal(v0, v1)
+        vis = [s.kv_rows(l, 0, s.length) for l in range(mc.n_layers)]
+        nxt = f[0].emitted()[-1]
+        _, f2 = eng.verify([sv.Request(s, 2, nxt, [1, 2, 3, 4])], exit_layer=0)
+        final_states.append((vis, f[0].asdict(), f2[0].asdict(),
+                             [s.kv_rows(l, 0, s.length) for l in range(mc.n_layers)]))
+        s.close()
+    A, B = final_states
+    for l in range(mc.n_layers):
+        assert np.array_equal(A[0][l][0], B[0][l][0]) and np.array_equal(A[0][l][1], B[0][l][1])
+        assert np.array_equal(A[3][l][0], B[3][l][0])
+    assert A[1]["tokens"] == B[1]["tokens"]
+    assert A[2] == B[2]
+    eng.close()
+
+
+def test_protocol_errors(svlib):
+    mc = tiny()
+    sv, W, eng = _setup(mc, 2)
+    s = eng.open_session(1, 1)
+    s.fill_kv(20, kv_seed=1)
+    _, f = eng.verify([sv.Request(s, 5, 1, [1, 2, 3, 4])])           # round 5 is not 0 + 1
+    assert f[0].status == sv.SV_E_PROTOCOL and s.length == 20
+    _, f = eng.verify([sv.Request(s, 1, 1, [1, 2, 3, 4], prefix_len=7)])
+    assert f[0].status == sv.SV_E_PROTOCOL and s.length == 20
+    q = np.full((4, mc.vocab), 1.0 / mc.vocab, dtype=np.float32)
+    q[3, 4] = 0.0
+    _, f = eng.verify([sv.Request(s, 1, 1, [1, 2, 3, 4], q)])          # host probs, q_4(x_4) = 0
+    assert f[0].status == sv.SV_E_PROTOCOL and s.length == 20
+    _, f = eng.verify([sv.Request(s, 1, 1, [1, 2, 3, 4])])
+    assert f[0].status == sv.SV_OK and s.length == 20 + 1 + f[0].accepted
+    with pytest.raises(sv.SvError):
+        eng.verify([sv.Request(s, 2, 1, [1, 2, 3, mc.vocab])])        # token out of range
+    s.close()
+    eng.close()
+
+
+def test_host_probs_equal_device_probs(svlib):
+    mc = tiny()
+    sv, W, eng = _setup(mc, 1)
+    out = []
+    for host in (True, False):
+        s = eng.open_session(3, 3)
+        s.fill_kv(20, kv_seed=1)
+        x, q = wd.timing_drafts(8, 1, 4, mc.vocab, s=1.1)
+        p = q[0] if host else torch.from_numpy(q[0]).cuda()
+        _, f = eng.verify([sv.Request(s, 1, 2, x[0], p)])
+        out.append(f[0].asdict())
+        s.close()
+    assert out[0] == out[1]
+    eng.close()
+
+
+def test_7b_width_two_layers(svlib):
+    """Llama2-7B layer shapes (d=4096, 32 heads, F=11008, V=32000) with 2 layers,
+    batch 2, ctx 200: logits and decisions vs the fp64 oracle."""
+    mc = ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=512)
+    tf, te, errs = _run_rounds(mc, 2, 4, 200, 1, False, rounds=2)
+    print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
+    assert errs.max() < LOGIT_TOL
+    assert not tf.hard_mismatch and not te.hard_mismatch
