@@ -1,0 +1,474 @@
+#!/usr/bin/env python
+"""bench.py — the verify-step benchmark of BASELINE.json.
+
+metric : "verify-step latency p50 and verified tokens/s, Llama2-7B shape gamma=4"
+value  : verified tokens/s of the whole job (sum over ranks of sum(delta+1) over
+         the timed steps / max over ranks of the device-timed region), inputs
+         resident in HBM.  `latency_p50_ms` is the device-timed p50 step latency.
+e2e    : the same metric through the public API with the draft distributions
+         copied from pinned host memory every step and results read back (host
+         wall clock, synchronised at both ends).
+
+A step = one pass of the whole hot path over one batch:
+embed, 32 decoder layers, early exit at layer l_e (LM head + acceptance on the
+exit stream), final LM head, acceptance and KV rollback.  The workload is kept
+stationary: before each step every session is rewound to its prefix length, so
+each timed step verifies the same (context, drafts) with fresh Philox counters
+(new round id).  Drafts are "Vicuna-68M-style" calibrated distributions:
+q_j = normalize(l*p_j + (1-l)*r_j), p_j the target row along the drafted path,
+r_j a Zipf(1.5) row over a random permutation, l chosen by bisection so that
+sum_v min(p_j, q_j) = alpha.
+
+--impl reference runs the oracle (numpy fp64, tests-only infrastructure) on the
+host cores on a bounded sample of the same workload.
+
+Launch: python bench.py [--gpus N --steps K --warmup W] (N>1 under torchrun;
+each rank runs its own requests, no collective on the hot path; NCCL gathers
+counters once at the end).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "verify-step latency p50 and verified tokens/s, Llama2-7B shape gamma=4"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4", "C5"])
+    ap.add_argument("--gamma", type=int, default=4)
+    ap.add_argument("--exit-layer", type=int, default=16)
+    ap.add_argument("--alpha", type=float, default=0.825)
+    ap.add_argument("--batch", type=int, default=None, help="requests per GPU (default: per config)")
+    ap.add_argument("--ctx", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-json", default=None, help="write per-launch profile records here")
+    return ap.parse_args()
+
+
+def workload(args, world):
+    """(requests on this GPU, total requests, ctx, scaling) for the config."""
+    if args.config in ("C2", "C3"):
+        per, ctx, scaling = 1, 512, "weak"
+    elif args.config == "C4":
+        per, ctx, scaling = 256 // world, 1024, "strong"
+    else:  # C5
+        per, ctx, scaling = max(1, 16 // world), 2048, "strong" if world > 1 else "weak"
+    if args.batch:
+        per = args.batch
+    if args.ctx:
+        ctx = args.ctx
+    return per, per * world, ctx, scaling
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-i", str(self.gpu),
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- helpers
+def softmax64(z):
+    z = np.asarray(z, dtype=np.float64)
+    e = np.exp(z - z.max())
+    return e / e.sum()
+
+
+def calibrate_row(p, r, alpha):
+    """lambda in [0,1] with sum_v min(p, l p + (1-l) r) = alpha (bisection)."""
+    f = lambda lam: np.minimum(p, lam * p + (1 - lam) * r).sum()
+    if f(0.0) >= alpha:
+        return 0.0
+    lo, hi = 0.0, 1.0
+    for _ in range(50):
+        mid = 0.5 * (lo + hi)
+        if f(mid) < alpha:
+            lo = mid
+        else:
+            hi = mid
+    return hi
+
+
+class Rounds:
+    def __init__(self):
+        self.r = {}
+
+    def next(self, s):
+        self.r[id(s)] = self.r.get(id(s), 0) + 1
+        return self.r[id(s)]
+
+
+def build_calibrated_drafts(sv, eng, sessions, pendings, ctx, gamma, alpha, V, seed, rounds):
+    """gamma sequential probe steps (greedy, rewound) to read the target rows along
+    the drafted path; returns (drafts int32 [B,gamma], q float32 [B,gamma,V], alpha_j)."""
+    from workload.drafts import zipf_rows
+    B = len(sessions)
+    rng = np.random.default_rng([seed, 99, B, gamma])
+    x = np.zeros((B, gamma), dtype=np.int32)
+    q = np.zeros((B, gamma, V), dtype=np.float32)
+    for j in range(gamma):
+        reqs = [sv.Request(s, rounds.next(s), pendings[b], x[b]) for b, s in enumerate(sessions)]
+        t = eng.submit(reqs, exit_layer=0)
+        t.wait_final()
+        z = t.logits(1, gamma)[:, j].double().cpu().numpy()
+        t.release()
+        for s in sessions:
+            s.rewind(ctx)
+        r = zipf_rows(rng, B, V, 1.5)
+        for b in range(B):
+            p = softmax64(z[b])
+            lam = calibrate_row(p, r[b], alpha)
+            qj = lam * p + (1 - lam) * r[b]
+            qj /= qj.sum()
+            cdf = np.cumsum(qj)
+            x[b, j] = min(int(np.searchsorted(cdf, rng.random() * cdf[-1])), V - 1)
+            q[b, j] = qj.astype(np.float32)
+    return x, q
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return d["hbm_gbs"], d.get("bf16_tflops_sustained"), "measured"
+    except Exception:
+        return 6650.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kind):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        d = json.load(open(path))
+        return d["dram_bytes_per_launch"].get(kind)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------- CPU side
+class OracleSample:
+    """Oracle verify step on a bounded sample of the workload: the Llama2-7B layer
+    shapes with 1 and 2 decoder layers (+ LM heads, acceptance), B=1, timed on the
+    host cores; one 32-layer step is extrapolated as t1 + 31 * (t2 - t1).
+    Weight generation happens once, outside the timed calls."""
+
+    def __init__(self, args, ctx):
+        from oracle import model as om
+        from workload.configs import ModelCfg
+        from workload.drafts import timing_drafts
+        self.args, self.ctx = args, ctx
+        self.models = {}
+        for L in (1, 2):
+            mc = ModelCfg(n_layers=L, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=ctx + 64)
+            self.models[L] = (om.Model(mc, seed=1), om.KVCache.synthetic(mc, 2, ctx))
+        self.x, self.q = timing_drafts(3, 1, args.gamma, 32000)
+        self.round = 0
+
+    def step(self):
+        from oracle.verify import Session as OSession
+        from oracle.verify import verify_step
+        t = {}
+        toks = []
+        self.round += 1
+        for L, (m, cache) in self.models.items():
+            sess = OSession(1, 4, cache.copy())
+            sess.last_round = self.round - 1
+            t0 = time.perf_counter()
+            out = verify_step(m, sess, self.round, 7, self.x[0], self.q[0].astype(np.float64), exit_layer=1)
+            t[L] = time.perf_counter() - t0
+            toks.append(out.final.accepted + 1)
+        self.t = t
+        return t[1] + 31 * max(t[2] - t[1], 1e-6), float(np.mean(toks))
+
+    def describe(self, t32):
+        return (f"oracle verify_step (numpy fp64) at Llama2-7B layer shapes, B=1, ctx {self.ctx}, "
+                f"gamma {self.args.gamma}, exit at layer 1, timed with 1 and 2 decoder layers "
+                f"({self.t[1]:.2f} s, {self.t[2]:.2f} s); 32-layer step extrapolated t1 + 31*(t2-t1) = "
+                f"{t32:.2f} s; weight generation excluded")
+
+
+def host_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    per, total, ctx, scaling = workload(args, 1)
+    sample = OracleSample(args, ctx)
+    times, toks = [], []
+    for i in range(args.warmup + args.steps):
+        t32, tps = sample.step()
+        if i >= args.warmup:
+            times.append(t32)
+            toks.append(tps)
+    sec = float(np.mean(times))
+    tok = float(np.mean(toks))
+    value = per * tok / sec
+    cores, desc = host_cores(), sample.describe(sec)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} Llama2-7B shape, B={per}, ctx {ctx}, gamma {args.gamma}",
+                       "global_batch": per, "seq_len": ctx, "parallelism": "host cores"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": desc + f"; tokens/step {tok:.3f} from the oracle's own decisions "
+                                       "(timing-mode Zipf drafts)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU side
+def run_ours(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_2505_21594_b200 import sv
+    from workload import llama2_7b
+    from workload.drafts import prefix_tokens
+
+    per, total, ctx, scaling = workload(args, world)
+    gamma, exit_layer = args.gamma, args.exit_layer
+    mc = llama2_7b()
+    W = sv.Weights(mc, seed=1, device=local)
+    blocks_per = (ctx + gamma + 1 + 63) // 64 + 1
+    eng = sv.Engine(mc, W, max_batch=per, max_gamma=gamma, kv_blocks=per * blocks_per, device=local)
+    sessions = []
+    for b in range(per):
+        rid = rank * per + b                       # request r -> GPU r // per (contiguous shard)
+        s = eng.open_session(rid + 1, 0x5EED0000 + rid)
+        s.fill_kv(ctx, kv_seed=1000 + rid)
+        sessions.append(s)
+    pend = prefix_tokens(3 + rank, per, mc.vocab)
+    rounds = Rounds()
+    x, q = build_calibrated_drafts(sv, eng, sessions, pend, ctx, gamma, args.alpha, mc.vocab, 7 + rank, rounds)
+    q_dev = torch.from_numpy(q).cuda()
+    q_pin = torch.from_numpy(q).pin_memory()
+    q_host = q_pin.numpy()
+    stream = torch.cuda.current_stream()
+
+    def step(host_probs=False):
+        for s in sessions:
+            s.rewind(ctx)
+        reqs = [sv.Request(s, rounds.next(s), pend[b], x[b], q_host[b] if host_probs else q_dev[b])
+                for b, s in enumerate(sessions)]
+        t = eng.submit(reqs, exit_layer=exit_layer, stream=stream)
+        if exit_layer:
+            t.wait_early()
+        f = t.wait_final()
+        t.release()
+        return sum(r.accepted + 1 for r in f), f
+
+    # warm-up (also captures the CUDA graph)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    tokens = 0
+    accepted_hist = np.zeros(gamma + 2, dtype=np.int64)
+    with ClockSampler(local) as clk:
+        t_all0 = torch.cuda.Event(enable_timing=True)
+        t_all1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t_all0.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            n_tok, f = step()
+            ev[i][1].record(stream)
+            tokens += n_tok
+            for r in f:
+                accepted_hist[r.accepted] += 1
+        t_all1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    elapsed = t_all0.elapsed_time(t_all1) / 1e3
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    launches = eng.last_launches()
+
+    # end to end: host probs (pinned) -> H2D inside each step, results D2H
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e2e_tok = 0
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        n_tok, _ = step(host_probs=True)
+        e2e_tok += n_tok
+    torch.cuda.synchronize()
+    e2e_el = time.perf_counter() - t0
+
+    # per-launch profile (events around each kernel, PDL off, no graph)
+    for s in sessions:
+        s.rewind(ctx)
+    preqs = [sv.Request(s, rounds.next(s), pend[b], x[b], q_dev[b]) for b, s in enumerate(sessions)]
+    _, recs = eng.profile_step(preqs, exit_layer=exit_layer)
+
+    # gather counters over ranks (the only collective)
+    stats = torch.tensor([tokens, elapsed, e2e_tok, e2e_el], dtype=torch.float64, device="cuda")
+    if dist:
+        allv = [torch.zeros_like(stats) for _ in range(world)]
+        dist.all_gather(allv, stats)
+        allv = torch.stack(allv).cpu().numpy()
+    else:
+        allv = stats.cpu().numpy()[None]
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    tot_tokens = allv[:, 0].sum()
+    t_max = allv[:, 1].max()
+    value = tot_tokens / t_max
+    e2e_value = allv[:, 2].sum() / allv[:, 3].max()
+
+    # roofline of the dominant kernel family (the weight-streaming GEMM)
+    hbm, tc, peak_src = measured_peaks()
+    fam = {}
+    for r in recs:
+        k = r["kind"]
+        f = fam.setdefault(k, [0.0, 0.0, 0])
+        f[0] += r["bytes"]
+        f[1] += r["ms"]
+        f[2] += 1
+    gemm_kinds = [k for k in fam if k.startswith("gemm")]
+    g_bytes = sum(fam[k][0] for k in gemm_kinds)
+    g_ms = sum(fam[k][1] for k in gemm_kinds)
+    g_n = sum(fam[k][2] for k in gemm_kinds)
+    step_ms_prof = sum(r["ms"] for r in recs)
+    achieved = g_bytes / (g_ms / 1e3) / 1e9
+    tr = ncu_traffic("gemm")
+    step_bytes = sum(r["bytes"] for r in recs)
+    roofline = {"bound": "hbm", "kernel": "gemm_kernel (QKV/O/gate-up/down/LM-head, tcgen05 + TMA)",
+                "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                "traffic": tr, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": g_bytes / g_n, "avg_launch_ms": g_ms / g_n,
+                "share_of_step": round(g_ms / step_ms_prof, 4),
+                "step_algorithmic_bytes": step_bytes,
+                "step_frac_of_peak": round(step_bytes / (statistics.median(step_ms) / 1e3) / 1e9 / hbm, 4),
+                "kernels": {k: {"launches": v[2], "ms": round(v[1], 4), "GB/s": round(v[0] / (v[1] / 1e3) / 1e9, 1)}
+                            for k, v in fam.items()}}
+    if args.profile_json:
+        json.dump({"records": recs, "step_ms": step_ms}, open(args.profile_json, "w"))
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        sample = OracleSample(args, ctx)
+        t32, _ = sample.step()
+        cores, desc = host_cores(), sample.describe(t32)
+        tps = tokens / args.steps
+        cpu = {"value": tps / t32, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": desc + f"; tokens/step {tps:.3f} taken from this workload's verified decisions"}
+
+    h2d = per * gamma * mc.vocab * 4 + per * (gamma + 1) * 12
+    d2h = 2 * per * 64
+    line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_max * 1e3 / args.steps, 4),
+            "latency_p50_ms": round(statistics.median(step_ms), 4),
+            "latency_p90_ms": round(float(np.percentile(step_ms, 90)), 4),
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init Llama2-7B-shape weights, synthetic KV, calibrated draft distributions)",
+            "config": {"workload": f"{args.config}: Llama2-7B shape (32 layers, d 4096, V 32000), "
+                                   f"{per} request(s)/GPU, ctx {ctx}, gamma {gamma}, early exit at layer "
+                                   f"{exit_layer}, stochastic acceptance, alpha {args.alpha}",
+                       "global_batch": total, "seq_len": ctx, "gamma": gamma, "exit_layer": exit_layer,
+                       "parallelism": f"requests sharded over {world} GPU(s), weights replicated",
+                       "l2": "inputs larger than L2 (13.5 GB of weights streamed per step)"},
+            "tokens_per_step": round(tot_tokens / (args.steps * total), 4),
+            "accepted_hist": accepted_hist.tolist(),
+            "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches * args.steps, "kernels_per_step": launches,
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

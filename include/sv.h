@@ -136,6 +136,10 @@ SV_API sv_status sv_session_open(sv_engine* e, uint64_t session_id, uint64_t phi
  * synthetic_kv), sets the cached length to len.  Synchronous. */
 SV_API sv_status sv_session_fill_kv(sv_session* s, int32_t len, uint64_t kv_seed);
 SV_API sv_status sv_session_len(const sv_session* s, int32_t* len);
+/* Client-driven rollback: make rows >= len invisible (0 <= len <= cached length).
+ * No data moves; the next step writes from position len.  The round counter is
+ * unchanged. */
+SV_API sv_status sv_session_rewind(sv_session* s, int32_t len);
 SV_API sv_status sv_session_close(sv_session* s);
 
 /* ---------------------------------------------------------------- verify ---- */
@@ -195,6 +199,24 @@ SV_API sv_status sv_debug_accept(sv_engine* e, const float* logits_dev, const sv
  * (bf16 [count][d_model], element [pos][head*head_dim + dim]).  Synchronous. */
 SV_API sv_status sv_debug_kv_rows(sv_session* s, int32_t layer, int32_t first, int32_t count,
                            void* k_host, void* v_host);
+/* Per-launch profile of one verify step: the step runs without graph replay and
+ * without programmatic dependent launch, each kernel bracketed by CUDA events on
+ * the stream it is launched on.  Commits like sv_verify (the caller may rewind).
+ * bytes / flops = algorithmic work of the launch. */
+enum {
+    SV_K_EMBED = 0, SV_K_QKV = 1, SV_K_ATTN = 2, SV_K_O = 3, SV_K_GU = 4, SV_K_DOWN = 5,
+    SV_K_LM_EXIT = 6, SV_K_ACCEPT_EXIT = 7, SV_K_LM_FINAL = 8, SV_K_ACCEPT_FINAL = 9
+};
+typedef struct {
+    int32_t kind;    /* SV_K_*                                   */
+    int32_t layer;   /* 0-based decoder layer, or -1             */
+    float ms;        /* event-measured duration                  */
+    double bytes;    /* algorithmic bytes read + written         */
+    double flops;    /* algorithmic floating-point operations    */
+} sv_kernel_prof;
+SV_API sv_status sv_debug_profile_step(sv_engine* e, const sv_verify_req* reqs, int32_t n, int32_t exit_layer,
+                                       sv_exit_result* early, sv_exit_result* final_, sv_kernel_prof* out,
+                                       int32_t cap, int32_t* n_out);
 /* Philox4x32-10 evaluated on the device (host in/out).  Synchronous. */
 SV_API sv_status sv_debug_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 

@@ -299,7 +299,7 @@ cudaError_t accept_launch(const AcceptArgs& a, cudaStream_t st) {
     cfg.blockDim = dim3(ACC_THREADS, 1, 1);
     cfg.stream = st;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = g_use_pdl ? 1 : 0;
     cfg.gridDim = dim3(a.B * a.G, a.nch, 1);
     cudaError_t e = cudaLaunchKernelEx(&cfg, row_stats_kernel, a);
     if (e != cudaSuccess) return e;

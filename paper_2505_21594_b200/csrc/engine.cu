@@ -131,6 +131,14 @@ extern "C" sv_status sv_weights_generate(const sv_model_cfg* c, const sv_weights
 }
 
 // ------------------------------------------------------------------ engine
+// profile mode: every launch bracketed by CUDA events on its own stream
+struct ProfRec {
+    int kind, layer;
+    cudaStream_t st;
+    cudaEvent_t a, b;
+    double bytes, flops;
+};
+
 struct sv_session {
     sv_engine* e;
     uint64_t id, seed;
@@ -208,10 +216,12 @@ struct sv_engine {
     uint64_t seq = 0;
     sv_ticket* inflight = nullptr;
     bool poisoned = false;
+    std::vector<ProfRec>* prof = nullptr;
     std::mutex mu;
 };
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
 
 static sv_status engine_alloc(sv_engine* e) {
     const int d = e->d, F = e->F, V = e->V, MP = e->MP;
@@ -477,15 +487,44 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
     const auto& tma = e->tm_act[tn];   // {u, attn_out, act, u_exit}
     int nl = 0;
     cudaError_t r;
-#define LAUNCH(x)                         \
-    do {                                  \
-        if ((r = (x)) != cudaSuccess) return r; \
-        ++nl;                             \
+    // algorithmic bytes / flops per launch: every operand
+    // the op must read or write once
+    const double Md = (double)M * d, W2 = 2.0;
+    auto gemm_bytes = [&](double N, double K, double out) { return N * K * W2 + M * K * W2 + out; };
+    auto pbeg = [&](cudaStream_t s) -> cudaEvent_t {
+        cudaEvent_t ev = nullptr;
+        if (e->prof) {
+            cudaEventCreate(&ev);
+            cudaEventRecord(ev, s);
+        }
+        return ev;
+    };
+    auto pend = [&](cudaEvent_t a, int kind, int layer, cudaStream_t s, double bytes, double flops) {
+        if (!e->prof) return;
+        cudaEvent_t b;
+        cudaEventCreate(&b);
+        cudaEventRecord(b, s);
+        e->prof->push_back(ProfRec{kind, layer, s, a, b, bytes, flops});
+    };
+#define LAUNCH(kind, layer, s, bytes, flops, x)         \
+    do {                                                \
+        cudaEvent_t _a = pbeg(s);                       \
+        if ((r = (x)) != cudaSuccess) return r;         \
+        ++nl;                                           \
+        pend(_a, kind, layer, s, bytes, flops);         \
     } while (0)
 
     EmbedArgs ea{(const int32_t*)(e->meta_dev + e->off_tok), e->embed, e->norm_attn[0], e->h, e->u, ssq_at(e, 0, 0), M,
                  e->MP, d};
-    LAUNCH(embed_launch(ea, st));
+    LAUNCH(SV_K_EMBED, -1, st, Md * 2 + d * 2 + Md * 6 + (d / 128) * M * 4.0, 0.0, embed_launch(ea, st));
+    double attn_bytes = Md * 6, attn_flops = 0;
+    {
+        const int32_t* ctxh = (const int32_t*)(e->meta_host + e->off_ctx);
+        for (int b = 0; b < n; ++b) {
+            attn_bytes += (double)(ctxh[b] + G) * d * 4;
+            for (int j = 0; j < G; ++j) attn_flops += 4.0 * (ctxh[b] + j + 1) * d;
+        }
+    }
 
     auto gemm = [&](int epi, const CUtensorMap& A, const CUtensorMap& B, int N, int K, GemmArgs a, cudaStream_t s,
                     bool exit_ws) -> cudaError_t {
@@ -500,9 +539,9 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
         GemmArgs a = base_args(e, M);
         a.ssq_in = ssq_at(e, is_exit ? exit_layer : L, 0);
         a.logits = is_exit ? e->logits_exit : e->logits_final;
-        cudaError_t q = gemm(EPI_LOGITS, e->tm_lm, is_exit ? tma[3] : tma[0], V, d, a, s, is_exit);
-        if (q != cudaSuccess) return q;
-        ++nl;
+        cudaError_t q;
+        LAUNCH(is_exit ? SV_K_LM_EXIT : SV_K_LM_FINAL, -1, s, gemm_bytes(V, d, (double)M * V * 4),
+               2.0 * M * V * d, gemm(EPI_LOGITS, e->tm_lm, is_exit ? tma[3] : tma[0], V, d, a, s, is_exit));
         AcceptArgs aa = {};
         aa.logits = a.logits;
         aa.req = (const ReqDev*)(e->meta_dev + e->off_reqdev);
@@ -513,9 +552,14 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
         aa.B = n; aa.G = G; aa.V = V; aa.nch = e->acc_nch; aa.chunk = e->acc_chunk;
         aa.exit_layer = is_exit ? exit_layer : L;
         aa.is_final = is_exit ? 0 : 1;
-        q = accept_launch(aa, s);
-        nl += 2;
-        return q;
+        {
+            cudaEvent_t _a = pbeg(s);
+            if ((q = accept_launch(aa, s)) != cudaSuccess) return q;
+            nl += 2;
+            pend(_a, is_exit ? SV_K_ACCEPT_EXIT : SV_K_ACCEPT_FINAL, -1, s,
+                 (double)M * V * 4 + (double)n * V * 8, 0.0);
+        }
+        return cudaSuccess;
     };
 
     for (int l = 0; l < L; ++l) {
@@ -524,7 +568,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             a.layer = l;
             a.ssq_in = ssq_at(e, l, 0);
             a.qbuf = e->qbuf;
-            LAUNCH(gemm(EPI_QKV, e->tm_qkv[l], tma[0], 3 * d, d, a, st, false));
+            LAUNCH(SV_K_QKV, l, st, gemm_bytes(3.0 * d, d, Md * 8 + (d / 128) * M * 4.0), 2.0 * M * 3.0 * d * d,
+                   gemm(EPI_QKV, e->tm_qkv[l], tma[0], 3 * d, d, a, st, false));
         }
         {   // attention
             AttnArgs aa = {};
@@ -536,18 +581,20 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             aa.B = n; aa.G = G; aa.n_heads = e->H; aa.head_dim = e->D; aa.d_model = d; aa.n_layers = L;
             aa.layer = l; aa.page_tokens = e->cfg.page_tokens; aa.nchunk = nchunk;
             aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)e->D));
-            LAUNCH(attn_launch(aa, st));
+            LAUNCH(SV_K_ATTN, l, st, attn_bytes, attn_flops, attn_launch(aa, st));
         }
         {   // O projection + residual
             GemmArgs a = base_args(e, M);
             a.h = e->h; a.g_out = e->norm_mlp[l]; a.u_out = e->u; a.ssq_out = ssq_at(e, l, 1);
-            LAUNCH(gemm(EPI_RESID, e->tm_o[l], tma[1], d, d, a, st, false));
+            LAUNCH(SV_K_O, l, st, gemm_bytes(d, d, Md * 10 + (d / 128) * M * 4.0), 2.0 * M * d * d,
+                   gemm(EPI_RESID, e->tm_o[l], tma[1], d, d, a, st, false));
         }
         {   // gate/up + SwiGLU
             GemmArgs a = base_args(e, M);
             a.ssq_in = ssq_at(e, l, 1);
             a.act = e->act;
-            LAUNCH(gemm(EPI_SWIGLU, e->tm_gu[l], tma[0], 2 * F, d, a, st, false));
+            LAUNCH(SV_K_GU, l, st, gemm_bytes(2.0 * F, d, (double)M * F * 2 + (d / 128) * M * 4.0),
+                   2.0 * M * 2.0 * F * d, gemm(EPI_SWIGLU, e->tm_gu[l], tma[0], 2 * F, d, a, st, false));
         }
         {   // down + residual (+ early-exit copy with the final gain)
             GemmArgs a = base_args(e, M);
@@ -559,7 +606,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
                 a.u_out2 = e->u_exit;
             }
             a.ssq_out = ssq_at(e, l + 1, 0);
-            LAUNCH(gemm(EPI_RESID, e->tm_down[l], tma[2], d, F, a, st, false));
+            LAUNCH(SV_K_DOWN, l, st, gemm_bytes(d, F, Md * (l + 1 == exit_layer ? 12 : 10) + (d / 128) * M * 4.0),
+                   2.0 * M * d * F, gemm(EPI_RESID, e->tm_down[l], tma[2], d, F, a, st, false));
         }
         if (l + 1 == exit_layer) {   // fork the early exit (S10-S11)
             if ((r = cudaEventRecord(e->ev_fork, st)) != cudaSuccess) return r;
@@ -588,7 +636,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
 static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk) {
     CK(cudaMemcpyAsync(e->meta_dev, e->meta_host, e->meta_bytes, cudaMemcpyHostToDevice, st));
     int nl = 0;
-    if (!e->opts.use_graphs) {
+    if (!e->opts.use_graphs || e->prof) {
         CK(issue_step(e, st, n, gamma, exit_layer, nchunk, &nl));
         e->last_launches = nl;
         return SV_OK;
@@ -906,5 +954,43 @@ extern "C" sv_status sv_debug_philox(const uint32_t ctr[4], const uint32_t key[2
     CK(philox_launch(d, d + 8, 0));
     CK(cudaMemcpy(out, d + 8, 16, cudaMemcpyDeviceToHost));
     CK(cudaFree(d));
+    return SV_OK;
+}
+
+extern "C" sv_status sv_session_rewind(sv_session* s, int32_t len) {
+    if (!s) return fail(SV_E_INVALID, "NULL session");
+    sv_engine* e = s->e;
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (s->busy) return fail(SV_E_BUSY, "session has a ticket in flight");
+    if (len < 0 || len > s->len) return fail(SV_E_INVALID, "rewind length must be in [0, cached length]");
+    s->len = len;   // rows >= len become invisible; their pages stay allocated
+    return SV_OK;
+}
+
+extern "C" sv_status sv_debug_profile_step(sv_engine* e, const sv_verify_req* reqs, int32_t n, int32_t exit_layer,
+                                           sv_exit_result* early, sv_exit_result* final_, sv_kernel_prof* out,
+                                           int32_t cap, int32_t* n_out) {
+    if (!e || !out || !n_out) return fail(SV_E_INVALID, "NULL argument");
+    std::vector<ProfRec> recs;
+    e->prof = &recs;
+    const bool pdl = g_use_pdl;
+    g_use_pdl = false;   // serialise kernels so events bracket exactly one launch
+    sv_ticket* t = nullptr;
+    sv_status s = sv_verify_submit(e, reqs, n, exit_layer, early, final_, nullptr, &t);
+    e->prof = nullptr;
+    g_use_pdl = pdl;
+    if (s) return s;
+    if ((s = sv_ticket_release(t))) return s;
+    CK(cudaDeviceSynchronize());
+    int k = 0;
+    for (auto& r : recs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        if (k < cap) out[k] = sv_kernel_prof{r.kind, r.layer, ms, r.bytes, r.flops};
+        ++k;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    *n_out = k;
     return SV_OK;
 }

@@ -10,6 +10,10 @@ namespace sv {
 
 typedef uint16_t bf16_raw_t;   // raw bf16 storage in host-visible structs
 
+// programmatic dependent launch on/off (off in profile mode so per-kernel events
+// do not overlap)
+extern bool g_use_pdl;
+
 // ----------------------------------------------------------------- GEMM (K1)
 enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_LOGITS = 3 };
 

@@ -5,6 +5,8 @@
 
 namespace sv {
 
+bool g_use_pdl = true;
+
 // K4: h^(0) = E[token] (Eq. 3), fp32 residual; u = bf16(h * g_attn[0]);
 // ssq[t][m] = sum of h^2 over the 128-column tile t (RMSNorm statistics for layer 1).
 __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ EmbedArgs a) {
@@ -33,7 +35,7 @@ cudaError_t embed_launch(const EmbedArgs& a, cudaStream_t st) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = g_use_pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, embed_kernel, a);
 }
 

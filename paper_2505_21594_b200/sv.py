@@ -65,6 +65,14 @@ class sv_exit_result(C.Structure):
                     new_len=self.new_len)
 
 
+class sv_kernel_prof(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("layer", C.c_int32), ("ms", C.c_float), ("bytes", C.c_double),
+                ("flops", C.c_double)]
+
+
+KERNEL_KINDS = ["embed", "gemm_qkv", "attention", "gemm_o", "gemm_gate_up", "gemm_down",
+                "gemm_lm_exit", "accept_exit", "gemm_lm_final", "accept_final"]
+
 EXPORTS = {
     # name: (restype, argtypes)
     "sv_status_str": (C.c_char_p, [C.c_int]),
@@ -81,6 +89,10 @@ EXPORTS = {
     "sv_session_fill_kv": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64]),
     "sv_session_len": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "sv_session_close": (C.c_int, [C.c_void_p]),
+    "sv_session_rewind": (C.c_int, [C.c_void_p, C.c_int32]),
+    "sv_debug_profile_step": (C.c_int, [C.c_void_p, C.POINTER(sv_verify_req), C.c_int32, C.c_int32,
+                                        C.POINTER(sv_exit_result), C.POINTER(sv_exit_result),
+                                        C.POINTER(sv_kernel_prof), C.c_int32, C.POINTER(C.c_int32)]),
     "sv_verify_submit": (C.c_int, [C.c_void_p, C.POINTER(sv_verify_req), C.c_int32, C.c_int32,
                                    C.POINTER(sv_exit_result), C.POINTER(sv_exit_result), C.c_void_p,
                                    C.POINTER(C.c_void_p)]),
@@ -207,6 +219,9 @@ class Session:
     def fill_kv(self, length: int, kv_seed: int):
         check(lib().sv_session_fill_kv(self.h, length, kv_seed))
 
+    def rewind(self, length: int):
+        check(lib().sv_session_rewind(self.h, length))
+
     def kv_rows(self, layer: int, first: int, count: int):
         """(K, V) bf16 bit patterns uint16 [count, d] of cached rows."""
         d = self.engine.mc.d_model
@@ -330,6 +345,19 @@ class Engine:
         out = (sv_exit_result * n)()
         check(lib().sv_debug_accept(self.h, C.c_void_p(logits.data_ptr()), arr, n, out))
         return [out[i] for i in range(n)]
+
+    def profile_step(self, reqs, exit_layer: int = 0, cap: int = 4096):
+        """One step with per-launch CUDA-event timing; returns (final results, records)."""
+        n = len(reqs)
+        arr = (sv_verify_req * n)(*[r.to_c() for r in reqs])
+        early = (sv_exit_result * n)()
+        final = (sv_exit_result * n)()
+        out = (sv_kernel_prof * cap)()
+        k = C.c_int32()
+        check(lib().sv_debug_profile_step(self.h, arr, n, exit_layer, early, final, out, cap, C.byref(k)))
+        recs = [dict(kind=KERNEL_KINDS[out[i].kind], layer=out[i].layer, ms=out[i].ms, bytes=out[i].bytes,
+                     flops=out[i].flops) for i in range(min(k.value, cap))]
+        return [final[i] for i in range(n)], recs
 
     def last_launches(self) -> int:
         n = C.c_int32()
