@@ -41,6 +41,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+N_SETS = 8
 METRIC = "verify-step latency p50 and verified tokens/s, Llama2-7B shape gamma=4"
 UNIT = "tokens/s"
 
@@ -317,16 +318,22 @@ def run_ours(args):
         sessions.append(s)
     pend = prefix_tokens(3 + rank, per, mc.vocab)
     rounds = Rounds()
-    x, q = build_calibrated_drafts(sv, eng, sessions, pend, ctx, gamma, args.alpha, mc.vocab, 7 + rank, rounds)
-    q_dev = torch.from_numpy(q).cuda()
-    q_pin = torch.from_numpy(q).pin_memory()
-    q_host = q_pin.numpy()
+    # N_SETS independent calibrated draft sets per request; step i verifies set i % N_SETS
+    sets = [build_calibrated_drafts(sv, eng, sessions, pend, ctx, gamma, args.alpha, mc.vocab,
+                                    7 + 1000 * rank + k, rounds) for k in range(N_SETS)]
+    xs = [x for x, _ in sets]
+    q_dev = [torch.from_numpy(q).cuda() for _, q in sets]
+    q_host = [torch.from_numpy(q).pin_memory().numpy() for _, q in sets]
     stream = torch.cuda.current_stream()
+    counter = [0]
 
     def step(host_probs=False):
+        k = counter[0] % N_SETS
+        counter[0] += 1
+        x = xs[k]
         for s in sessions:
             s.rewind(ctx)
-        reqs = [sv.Request(s, rounds.next(s), pend[b], x[b], q_host[b] if host_probs else q_dev[b])
+        reqs = [sv.Request(s, rounds.next(s), pend[b], x[b], q_host[k][b] if host_probs else q_dev[k][b])
                 for b, s in enumerate(sessions)]
         t = eng.submit(reqs, exit_layer=exit_layer, stream=stream)
         if exit_layer:
@@ -379,7 +386,7 @@ def run_ours(args):
     # per-launch profile (events around each kernel, PDL off, no graph)
     for s in sessions:
         s.rewind(ctx)
-    preqs = [sv.Request(s, rounds.next(s), pend[b], x[b], q_dev[b]) for b, s in enumerate(sessions)]
+    preqs = [sv.Request(s, rounds.next(s), pend[b], xs[0][b], q_dev[0][b]) for b, s in enumerate(sessions)]
     _, recs = eng.profile_step(preqs, exit_layer=exit_layer)
 
     # gather counters over ranks (the only collective)

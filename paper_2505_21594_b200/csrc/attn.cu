@@ -3,7 +3,8 @@
 // For request b, head h and query row j (position ctx_b + j) the kernel computes
 //   a_j = softmax(q_j K^T / sqrt(Dh)) V   over keys 0 .. ctx_b + j      (Eq. 3 block)
 // Split-KV ("flash-decoding"): one CTA per (request, head, 64-key page); each CTA
-// stages its K and V page in shared memory with 16-byte loads, computes the
+// stages its K and V page in shared memory (all 16-byte loads of the page issued
+// before the first store, so a page costs one memory round trip), computes the
 // G x 64 score block, a page-local max / sum (log2 domain) and the partial
 // P.V, and writes (m, l, o) partials.  The last CTA of a (request, head)
 // (atomic ticket) merges the pages in page order 0..n-1 — a fixed order, so the
@@ -18,15 +19,19 @@ namespace sv {
 
 constexpr int KPAGE = 64;     // keys per page (= page_tokens)
 constexpr int GMAX = SV_MAX_GAMMA + 1;
+constexpr int MAXCH = 64;     // pages per request (ctx <= 4096)
 
 template <int D>
 __global__ void __launch_bounds__(128) attn_kernel(const __grid_constant__ AttnArgs a) {
     constexpr int KST = D + 8;                 // padded K row (bf16) -> conflict-free 16 B reads
+    constexpr int VPR = D / 8;                 // 16-byte vectors per row
+    constexpr int NV = KPAGE * VPR / 128;      // vectors per thread for a full page
     __shared__ __align__(16) bf16 sK[KPAGE * KST];
     __shared__ __align__(16) bf16 sV[KPAGE * D];
     __shared__ __align__(16) float sQ[GMAX * D];
     __shared__ float sS[GMAX * KPAGE];
     __shared__ float sM[GMAX], sL[GMAX];
+    __shared__ float sW[GMAX * MAXCH], sLc[GMAX * MAXCH];
     __shared__ int s_last;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -49,17 +54,36 @@ __global__ void __launch_bounds__(128) attn_kernel(const __grid_constant__ AttnA
                      (((size_t)blk * a.n_layers + a.layer) * 2 + 0) * plane + (size_t)h * a.page_tokens * D;
     const bf16* Vp = Kp + plane;
 
-    constexpr int VPR = D / 8;                 // 16-byte vectors per row
-    for (int v = tid; v < nk * VPR; v += 128) {
-        const int key = v / VPR, part = v % VPR;
-        const uint4 kx = __ldg(reinterpret_cast<const uint4*>(Kp + (size_t)key * D) + part);
-        const uint4 vx = __ldg(reinterpret_cast<const uint4*>(Vp + (size_t)key * D) + part);
-        *reinterpret_cast<uint4*>(&sK[key * KST + part * 8]) = kx;
-        *reinterpret_cast<uint4*>(&sV[key * D + part * 8]) = vx;
-    }
-    for (int i = tid; i < G * D; i += 128) {
-        const int j = i / D, dd = i % D;
-        sQ[j * D + dd] = a.q[(size_t)(b * G + j) * a.d_model + h * D + dd] * a.scale_log2;
+    {
+        uint4 kr[NV], vr[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int v = tid + i * 128, key = v / VPR, part = v % VPR;
+            if (key < nk) {
+                kr[i] = __ldg(reinterpret_cast<const uint4*>(Kp + (size_t)key * D) + part);
+                vr[i] = __ldg(reinterpret_cast<const uint4*>(Vp + (size_t)key * D) + part);
+            }
+        }
+        constexpr int QN = (GMAX * D + 127) / 128;
+        float qv[QN];
+#pragma unroll
+        for (int i = 0; i < QN; ++i) {
+            const int e = tid + i * 128, j = e / D, dd = e % D;
+            qv[i] = (j < G) ? a.q[(size_t)(b * G + j) * a.d_model + h * D + dd] : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const int v = tid + i * 128, key = v / VPR, part = v % VPR;
+            if (key < nk) {
+                *reinterpret_cast<uint4*>(&sK[key * KST + part * 8]) = kr[i];
+                *reinterpret_cast<uint4*>(&sV[key * D + part * 8]) = vr[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < QN; ++i) {
+            const int e = tid + i * 128;
+            if (e < GMAX * D) sQ[e] = qv[i] * a.scale_log2;
+        }
     }
     __syncthreads();
 
@@ -122,22 +146,45 @@ __global__ void __launch_bounds__(128) attn_kernel(const __grid_constant__ AttnA
     pdl_launch_dependents();
     if (!s_last) return;
     __threadfence();
-    // merge the pages of (b, h) in page order
+    // merge the pages of (b, h) in page order: (1) all (m, l) pairs in parallel
+    const size_t mbase = (size_t)bh * a.nchunk * G;
+    for (int i = tid; i < nch_b * G; i += 128) {
+        const int cc = i / G, j = i % G;
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(&a.part_ml[(mbase + (size_t)cc * G + j) * 2]));
+        sW[j * MAXCH + cc] = ml.x;
+        sLc[j * MAXCH + cc] = ml.y;
+    }
+    __syncthreads();
+    // (2) per row: M = max_c m_c, w_c = 2^(m_c - M), L = sum_c l_c w_c (page order)
+    if (tid < G) {
+        float M = -INFINITY;
+        for (int cc = 0; cc < nch_b; ++cc) M = fmaxf(M, sW[tid * MAXCH + cc]);
+        float L = 0.f;
+        for (int cc = 0; cc < nch_b; ++cc) {
+            const float m = sW[tid * MAXCH + cc];
+            const float w = (m == -INFINITY) ? 0.f : exp2f(m - M);
+            sW[tid * MAXCH + cc] = w;
+            L = fmaf(sLc[tid * MAXCH + cc], w, L);
+        }
+        sL[tid] = L;
+    }
+    __syncthreads();
+    // (3) O = sum_c w_c o_c / L, loads of 8 pages in flight
     for (int i = tid; i < G * D; i += 128) {
         const int j = i / D, e = i % D;
-        float M = -INFINITY;
-        for (int cc = 0; cc < nch_b; ++cc)
-            M = fmaxf(M, __ldcg(&a.part_ml[(((size_t)bh * a.nchunk + cc) * G + j) * 2]));
-        float L = 0.f, O = 0.f;
-        for (int cc = 0; cc < nch_b; ++cc) {
-            const size_t pj = ((size_t)bh * a.nchunk + cc) * G + j;
-            const float m = __ldcg(&a.part_ml[pj * 2]);
-            if (m == -INFINITY) continue;
-            const float w = exp2f(m - M);
-            L = fmaf(__ldcg(&a.part_ml[pj * 2 + 1]), w, L);
-            O = fmaf(__ldcg(&a.part_o[pj * D + e]), w, O);
+        const float* po = a.part_o + (mbase + j) * D + e;
+        const size_t cs = (size_t)G * D;       // page stride in part_o
+        float O = 0.f;
+        int cc = 0;
+        for (; cc + 8 <= nch_b; cc += 8) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(po + (cc + u) * cs);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) O = fmaf(v[u], sW[j * MAXCH + cc + u], O);
         }
-        reinterpret_cast<bf16*>(a.out)[(size_t)(b * G + j) * a.d_model + h * D + e] = __float2bfloat16_rn(O / L);
+        for (; cc < nch_b; ++cc) O = fmaf(__ldcg(po + cc * cs), sW[j * MAXCH + cc], O);
+        reinterpret_cast<bf16*>(a.out)[(size_t)(b * G + j) * a.d_model + h * D + e] = __float2bfloat16_rn(O / sL[j]);
     }
     if (tid == 0) a.counters[bh] = 0;
 }
@@ -157,7 +204,7 @@ static cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
 }
 
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st) {
-    if (a.page_tokens != KPAGE || a.G > GMAX) return cudaErrorInvalidValue;
+    if (a.page_tokens != KPAGE || a.G > GMAX || a.nchunk > MAXCH) return cudaErrorInvalidValue;
     switch (a.head_dim) {
         case 32: return launch_d<32>(a, st);
         case 64: return launch_d<64>(a, st);

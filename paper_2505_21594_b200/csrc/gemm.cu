@@ -270,16 +270,37 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     if (!*s_flag) return;
     __threadfence();
+    const size_t sstride = (size_t)NT * a.MP * TM;     // distance between two splits' partials
     for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
         if (m0 + c0 >= a.M) break;
-        for (int j = 0; j < EPI_CHUNK; ++j) {
-            const int tok = m0 + c0 + j;
-            float acc = 0.f;
-            if (tok < a.M)
-                for (int s = 0; s < a.splits; ++s)
-                    acc += __ldcg(&a.ws[(((size_t)s * NT + nt) * a.MP + tok) * TM + row]);
-            sOut[j * TM + row] = acc;
+        const int nv = min(EPI_CHUNK, a.M - (m0 + c0));
+        // acc[j] = ((p_0 + p_1) + p_2) + ... in split order; the loads of 4 splits x
+        // all valid tokens are issued before any add (the sum order is unchanged)
+        float acc[EPI_CHUNK];
+#pragma unroll
+        for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = 0.f;
+        const float* base = a.ws + ((size_t)nt * a.MP + m0 + c0) * TM + row;
+        int s = 0;
+        for (; s + 4 <= a.splits; s += 4) {
+            float v[EPI_CHUNK][4];
+#pragma unroll
+            for (int j = 0; j < EPI_CHUNK; ++j)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[j][u] = (j < nv) ? __ldcg(base + (s + u) * sstride + j * TM) : 0.f;
+#pragma unroll
+            for (int j = 0; j < EPI_CHUNK; ++j)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc[j] += v[j][u];
         }
+        for (; s < a.splits; ++s) {
+            float v[EPI_CHUNK];
+#pragma unroll
+            for (int j = 0; j < EPI_CHUNK; ++j) v[j] = (j < nv) ? __ldcg(base + s * sstride + j * TM) : 0.f;
+#pragma unroll
+            for (int j = 0; j < EPI_CHUNK; ++j) acc[j] += v[j];
+        }
+#pragma unroll
+        for (int j = 0; j < EPI_CHUNK; ++j) sOut[j * TM + row] = acc[j];
         __syncthreads();
         epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt);
         __syncthreads();
