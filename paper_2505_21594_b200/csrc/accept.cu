@@ -78,6 +78,7 @@ __device__ __forceinline__ Stat stat_shfl(const Stat& s, int o) {
 
 __global__ void __launch_bounds__(ACC_THREADS) row_stats_kernel(const __grid_constant__ AcceptArgs a) {
     __shared__ Stat sW[ACC_THREADS / 32];
+    pdl_launch_dependents();
     pdl_wait();
     const int row = blockIdx.x, c = blockIdx.y;
     const int b = row / a.G;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(ACC_THREADS) accept_kernel(const __grid_consta
     __shared__ float s_margin;
     __shared__ Race sW[ACC_THREADS / 32];
 
+    pdl_launch_dependents();
     pdl_wait();
     const int b = blockIdx.x, c = blockIdx.y;
     const int G = a.G, gamma = G - 1, V = a.V;

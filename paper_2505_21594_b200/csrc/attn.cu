@@ -38,14 +38,12 @@ __global__ void __launch_bounds__(128) attn_kernel(const __grid_constant__ AttnA
     const int bh = blockIdx.x, c = blockIdx.y;
     const int b = bh / a.n_heads, h = bh % a.n_heads;
     const int G = a.G;
+    pdl_launch_dependents();   // the next GEMM may start streaming its weights now
     pdl_wait();
     const int ctx = a.ctx[b];
     const int T = ctx + G;
     const int nch_b = (T + KPAGE - 1) / KPAGE;
-    if (c >= nch_b) {
-        pdl_launch_dependents();
-        return;
-    }
+    if (c >= nch_b) return;
     const int k0 = c * KPAGE;
     const int nk = min(KPAGE, T - k0);
     const int blk = a.page_table[b * a.pt_stride + c];
@@ -143,7 +141,6 @@ __global__ void __launch_bounds__(128) attn_kernel(const __grid_constant__ AttnA
     __syncthreads();
     if (tid == 0) s_last = (atomicAdd(&a.counters[bh], 1) == nch_b - 1);
     __syncthreads();
-    pdl_launch_dependents();
     if (!s_last) return;
     __threadfence();
     // merge the pages of (b, h) in page order: (1) all (m, l) pairs in parallel

@@ -3,10 +3,11 @@
 set -euo pipefail
 HERE="$(cd "$(dirname "$0")" && pwd)"
 OUT="${1:-$HERE/../libsv.so}"
+shift || true
 NVCC="${NVCC:-/usr/local/cuda/bin/nvcc}"
 FLAGS=(-std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a
        -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -shared -cudart static
-       -Xptxas -v --expt-relaxed-constexpr)
+       -Xptxas -v --expt-relaxed-constexpr "$@")
 "$NVCC" "${FLAGS[@]}" -o "$OUT" \
   "$HERE/engine.cu" "$HERE/gemm.cu" "$HERE/attn.cu" "$HERE/accept.cu" "$HERE/misc.cu" 2> "$HERE/../build.log" \
   || { cat "$HERE/../build.log"; exit 1; }

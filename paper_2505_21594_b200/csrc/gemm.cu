@@ -43,17 +43,22 @@ constexpr int BK = 64;                      // K elements per stage (one 128 B s
 constexpr int TM = 128;                     // weight rows per tile (UMMA M)
 constexpr int A_STAGE = TM * BK * 2;        // 16 KB
 constexpr int EPI_CHUNK = 16;               // token columns per epilogue pass
+#ifndef SV_GEMM_CTAS_PER_SM
+#define SV_GEMM_CTAS_PER_SM 4
+#endif
 
 template <int TN>
 struct GemmCfg {
     static constexpr int B_STAGE = TN * BK * 2;
     static constexpr int STAGE = A_STAGE + B_STAGE;
-    // small token tiles: 2 CTAs per SM (<= 113 KB each), else 1 CTA per SM
-    static constexpr int BUDGET = (TN <= 64 ? 113 * 1024 : 225 * 1024) - 1024 - 4096;
+    // small token tiles: SV_GEMM_CTAS_PER_SM CTAs per SM (two grids co-resident
+    // under programmatic dependent launch), else 1 CTA per SM
+    static constexpr int AUX = 2048;        // barriers, tmem slot, rstd[TN], reductions
+    static constexpr int BUDGET =
+        (TN <= 64 ? (228 * 1024) / SV_GEMM_CTAS_PER_SM - 1024 : 225 * 1024) - 1024 - AUX;
     static constexpr int STAGES_RAW = BUDGET / STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static constexpr int TMEM_COLS = TN < 32 ? 32 : TN;
-    static constexpr int AUX = 4096;        // barriers, tmem slot, rstd[TN], reductions
     static constexpr int SMEM = 1024 + STAGES * STAGE + AUX;
     static_assert(STAGES >= 2, "pipeline too shallow");
     static_assert(EPI_CHUNK * TM * 4 <= STAGES * STAGE, "epilogue tile must fit the ring");
@@ -179,6 +184,10 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // let the next kernel's CTAs become resident now: they set up and start
+    // streaming their weights while this grid runs (their griddepcontrol.wait
+    // still waits for this grid's completion before touching activations)
+    pdl_launch_dependents();
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer
@@ -222,7 +231,15 @@ __global__ void __launch_bounds__(128, 1)
         float rs = 1.0f;
         if (a.ssq_in && tok < a.M) {
             float s = 0.f;
-            for (int k = 0; k < a.ssq_tiles; ++k) s += a.ssq_in[(size_t)k * a.MP + tok];
+            int k = 0;
+            for (; k + 8 <= a.ssq_tiles; k += 8) {   // 8 loads in flight, summed in tile order
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = a.ssq_in[(size_t)(k + u) * a.MP + tok];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) s += v[u];
+            }
+            for (; k < a.ssq_tiles; ++k) s += a.ssq_in[(size_t)k * a.MP + tok];
             rs = 1.0f / sqrtf(s * a.inv_d + a.eps);
         }
         sR[t] = rs;
@@ -230,7 +247,6 @@ __global__ void __launch_bounds__(128, 1)
 
     mbar_wait(done, 0);
     tc_fence_after();
-    pdl_launch_dependents();
 
     const int row = warp * 32 + lane;
     const uint32_t tbase = tmem + (static_cast<uint32_t>(warp * 32) << 16);

@@ -11,6 +11,7 @@ bool g_use_pdl = true;
 // ssq[t][m] = sum of h^2 over the 128-column tile t (RMSNorm statistics for layer 1).
 __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ EmbedArgs a) {
     __shared__ float sRed[4];
+    pdl_launch_dependents();
     pdl_wait();
     const int m = blockIdx.x, t = blockIdx.y;
     const int k = t * 128 + threadIdx.x;
@@ -22,7 +23,6 @@ __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ Embe
     const float s = warp_sum(hv * hv);
     if ((threadIdx.x & 31) == 0) sRed[threadIdx.x >> 5] = s;
     __syncthreads();
-    pdl_launch_dependents();
     if (threadIdx.x == 0) a.ssq[(size_t)t * a.MP + m] = (sRed[0] + sRed[1]) + (sRed[2] + sRed[3]);
 }
 

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsv.so")
+LIB_PATH = os.environ.get("SV_LIB", os.path.join(_HERE, "libsv.so"))
 
 SV_MAX_GAMMA = 8
 SV_OK, SV_E_INVALID, SV_E_PROTOCOL, SV_E_CAPACITY, SV_E_DEVICE, SV_E_BUSY, SV_E_TIMEOUT = range(7)
