@@ -301,6 +301,7 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     from paper_2505_21594_b200 import sv
+    from paper_2505_21594_b200.dist import gather_counters, shard
     from workload import llama2_7b
     from workload.drafts import prefix_tokens
 
@@ -311,8 +312,7 @@ def run_ours(args):
     blocks_per = (ctx + gamma + 1 + 63) // 64 + 1
     eng = sv.Engine(mc, W, max_batch=per, max_gamma=gamma, kv_blocks=per * blocks_per, device=local)
     sessions = []
-    for b in range(per):
-        rid = rank * per + b                       # request r -> GPU r // per (contiguous shard)
+    for rid in shard(total, world, rank):          # contiguous shard of the request ids
         s = eng.open_session(rid + 1, 0x5EED0000 + rid)
         s.fill_kv(ctx, kv_seed=1000 + rid)
         sessions.append(s)
@@ -390,13 +390,7 @@ def run_ours(args):
     _, recs = eng.profile_step(preqs, exit_layer=exit_layer)
 
     # gather counters over ranks (the only collective)
-    stats = torch.tensor([tokens, elapsed, e2e_tok, e2e_el], dtype=torch.float64, device="cuda")
-    if dist:
-        allv = [torch.zeros_like(stats) for _ in range(world)]
-        dist.all_gather(allv, stats)
-        allv = torch.stack(allv).cpu().numpy()
-    else:
-        allv = stats.cpu().numpy()[None]
+    allv = gather_counters([tokens, elapsed, e2e_tok, e2e_el], device="cuda")
     if rank != 0:
         if dist:
             dist.destroy_process_group()

@@ -44,7 +44,7 @@ constexpr int TM = 128;                     // weight rows per tile (UMMA M)
 constexpr int A_STAGE = TM * BK * 2;        // 16 KB
 constexpr int EPI_CHUNK = 16;               // token columns per epilogue pass
 #ifndef SV_GEMM_CTAS_PER_SM
-#define SV_GEMM_CTAS_PER_SM 4
+#define SV_GEMM_CTAS_PER_SM 2
 #endif
 
 template <int TN>
