@@ -118,6 +118,9 @@ typedef struct {
     int32_t max_batch;   /* max requests per submit (>= 1)                          */
     int32_t max_gamma;   /* max draft length per submit (1..SV_MAX_GAMMA)           */
     int32_t use_graphs;  /* 1: replay one CUDA graph per (batch, gamma, exit, ctx)  */
+    int32_t fused;       /* 1: the whole step is ONE persistent kernel (one CTA per
+                            SM, stream-K GEMM segments, device-side dependency
+                            counters); 0: one kernel per op       */
 } sv_engine_opts;
 
 /* kv_pool: device memory (caller-owned, >= one KV block), carved into blocks of
@@ -205,7 +208,8 @@ SV_API sv_status sv_debug_kv_rows(sv_session* s, int32_t layer, int32_t first, i
  * bytes / flops = algorithmic work of the launch. */
 enum {
     SV_K_EMBED = 0, SV_K_QKV = 1, SV_K_ATTN = 2, SV_K_O = 3, SV_K_GU = 4, SV_K_DOWN = 5,
-    SV_K_LM_EXIT = 6, SV_K_ACCEPT_EXIT = 7, SV_K_LM_FINAL = 8, SV_K_ACCEPT_FINAL = 9
+    SV_K_LM_EXIT = 6, SV_K_ACCEPT_EXIT = 7, SV_K_LM_FINAL = 8, SV_K_ACCEPT_FINAL = 9,
+    SV_K_FUSED = 10   /* the whole step as one persistent kernel (opts.fused) */
 };
 typedef struct {
     int32_t kind;    /* SV_K_*                                   */

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "../../include/sv.h"
+#include "fused.h"
 #include "kernels.h"
 
 using namespace sv;
@@ -204,6 +205,11 @@ struct sv_engine {
     // pinned mailboxes
     sv_exit_result *mb_exit, *mb_final;
     volatile uint64_t* mb_flag;
+    sv_exit_result* mb_exit_dev = nullptr;      // device aliases of the mapped mailboxes
+    uint64_t* mb_flag_dev = nullptr;
+    // fused persistent step: device-resident tensor maps and per-key plans
+    CUtensorMap* d_tmaps = nullptr;             // [4L+1 weights][5 tile sizes x 4 activation maps]
+    std::map<StepKey, FusedPlan*> plans;
     // tensor maps
     std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;
     CUtensorMap tm_lm;
@@ -299,10 +305,12 @@ static sv_status engine_alloc(sv_engine* e) {
     CK(dalloc((void**)&e->meta_dev, off));
     CK(cudaMallocHost((void**)&e->meta_host, off));
     memset(e->meta_host, 0, off);
-    CK(cudaMallocHost((void**)&e->mb_exit, (size_t)B * sizeof(sv_exit_result)));
+    CK(cudaHostAlloc((void**)&e->mb_exit, (size_t)B * sizeof(sv_exit_result), cudaHostAllocMapped));
     CK(cudaMallocHost((void**)&e->mb_final, (size_t)B * sizeof(sv_exit_result)));
-    CK(cudaMallocHost((void**)&e->mb_flag, 64));
+    CK(cudaHostAlloc((void**)&e->mb_flag, 64, cudaHostAllocMapped));
     *e->mb_flag = 0;
+    CK(cudaHostGetDevicePointer((void**)&e->mb_exit_dev, e->mb_exit, 0));
+    CK(cudaHostGetDevicePointer((void**)&e->mb_flag_dev, (void*)e->mb_flag, 0));
     return SV_OK;
 }
 
@@ -325,7 +333,37 @@ static sv_status engine_tmaps(sv_engine* e) {
             return fail(SV_E_DEVICE, "tensor map (activations)");
         e->tm_act[tn] = m;
     }
+    // device copy for the fused kernel: weights [qkv L][o L][gu L][down L][lm], then
+    // activation maps at 4L+1 + 4*ti + k (ti = index of the tile size, k = buffer)
+    const int L = e->L, nmaps = 4 * L + 1 + 20;
+    std::vector<CUtensorMap> all(nmaps);
+    memset(all.data(), 0, sizeof(CUtensorMap) * nmaps);
+    for (int l = 0; l < L; ++l) {
+        all[l] = e->tm_qkv[l];
+        all[L + l] = e->tm_o[l];
+        all[2 * L + l] = e->tm_gu[l];
+        all[3 * L + l] = e->tm_down[l];
+    }
+    all[4 * L] = e->tm_lm;
+    int ti = 0;
+    for (int tn : {16, 32, 64, 128, 256}) {
+        auto it = e->tm_act.find(tn);
+        if (it != e->tm_act.end())
+            for (int k = 0; k < 4; ++k) all[4 * L + 1 + 4 * ti + k] = it->second[k];
+        ++ti;
+    }
+    CK(cudaMalloc((void**)&e->d_tmaps, sizeof(CUtensorMap) * nmaps));
+    CK(cudaMemcpy(e->d_tmaps, all.data(), sizeof(CUtensorMap) * nmaps, cudaMemcpyHostToDevice));
     return SV_OK;
+}
+
+static const CUtensorMap* dev_act_map(sv_engine* e, int tn, int k) {
+    int ti = 0;
+    for (int t : {16, 32, 64, 128, 256}) {
+        if (t == tn) break;
+        ++ti;
+    }
+    return e->d_tmaps + 4 * e->L + 1 + 4 * ti + k;
 }
 
 extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights* w, const sv_engine_opts* opts,
@@ -374,6 +412,11 @@ extern "C" sv_status sv_engine_destroy(sv_engine* e) {
     cudaSetDevice(e->device);
     cudaDeviceSynchronize();
     for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : e->plans) {
+        fused_free(kv.second);
+        delete kv.second;
+    }
+    if (e->d_tmaps) cudaFree(e->d_tmaps);
     void* dev[] = {e->h, e->qbuf, e->ssq, e->logits_exit, e->logits_final, e->ws_main, e->ws_exit, e->rope,
                    e->attn_o, e->attn_ml, e->u, e->u_exit, e->attn_out, e->act, e->cnt_main, e->cnt_exit,
                    e->cnt_attn, e->cnt_acc_exit, e->cnt_acc_final, e->stats_exit, e->stats_final, e->race_exit,
@@ -479,9 +522,13 @@ static float* ssq_at(sv_engine* e, int layer, int which) {   // norm point (laye
     return e->ssq + (size_t)(2 * layer + which) * (e->d / 128) * e->MP;
 }
 
+static cudaError_t issue_fused(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk,
+                               int* launches);
+
 // Issues every kernel / copy of one step on (main, exit) streams; returns launch count.
 static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk,
                               int* launches) {
+    if (e->opts.fused) return issue_fused(e, st, n, gamma, exit_layer, nchunk, launches);
     const int G = gamma + 1, M = n * G, d = e->d, F = e->F, V = e->V, L = e->L;
     const int tn = gemm_pick_tile_n(M);
     const auto& tma = e->tm_act[tn];   // {u, attn_out, act, u_exit}
@@ -631,6 +678,181 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
 #undef LAUNCH
     *launches = nl;
     return cudaSuccess;
+}
+
+// ------------------------------------------------------------ fused step plan
+// Same ops, same epilogue arguments as issue_step, expressed as stages of the
+// persistent kernel (fused.cu).  Also returns the step's algorithmic bytes /
+// flops (the same per-op formulas as the per-op profile).
+static cudaError_t build_fused_plan(sv_engine* e, int n, int gamma, int exit_layer, int nchunk, FusedPlan* P,
+                                    double* bytes, double* flops) {
+    const int G = gamma + 1, M = n * G, d = e->d, F = e->F, V = e->V, L = e->L;
+    const int tn = gemm_pick_tile_n(M), MT = (M + tn - 1) / tn;
+    const double Md = (double)M * d;
+    double B = 0, FL = 0;
+    std::vector<FStage> st;
+    auto add = [&](const FStage& s) {
+        st.push_back(s);
+        return (int)st.size() - 1;
+    };
+    auto gemm_stage = [&](int epi, const CUtensorMap* A, const CUtensorMap* Bm, int N, int K, const GemmArgs& g,
+                          int dep, double out_bytes) {
+        FStage s;
+        memset(&s, 0, sizeof(s));
+        s.type = IT_GEMM;
+        s.dep = dep;
+        s.epi = epi;
+        s.nt_n = N / 128;
+        s.nt_m = MT;
+        s.kblocks = K / 64;
+        s.tmA = A;
+        s.tmB = Bm;
+        s.g = g;
+        s.g.N = N;
+        s.g.K = K;
+        s.g.splits = 1;
+        B += (double)N * K * 2 + (double)M * K * 2 + out_bytes;
+        FL += 2.0 * M * N * K;
+        return s;
+    };
+    auto accept_stage = [&](bool is_exit, int dep, bool stats) {
+        FStage s;
+        memset(&s, 0, sizeof(s));
+        s.type = stats ? IT_STATS : IT_ACCEPT;
+        s.dep = dep;
+        s.is_exit = is_exit ? 1 : 0;
+        AcceptArgs& aa = s.ac;
+        aa.logits = is_exit ? e->logits_exit : e->logits_final;
+        aa.req = (const ReqDev*)(e->meta_dev + e->off_reqdev);
+        aa.stats = is_exit ? e->stats_exit : e->stats_final;
+        aa.race = is_exit ? e->race_exit : e->race_final;
+        aa.counters = is_exit ? e->cnt_acc_exit : e->cnt_acc_final;
+        aa.out = is_exit ? e->res_exit_dev : e->res_final_dev;
+        aa.B = n; aa.G = G; aa.V = V; aa.nch = e->acc_nch; aa.chunk = e->acc_chunk;
+        aa.exit_layer = is_exit ? exit_layer : L;
+        aa.is_final = is_exit ? 0 : 1;
+        B += stats ? (double)M * V * 4 : (double)n * V * 8;
+        return s;
+    };
+    const CUtensorMap* tu = dev_act_map(e, tn, 0);
+    const CUtensorMap* ta = dev_act_map(e, tn, 1);
+    const CUtensorMap* tact = dev_act_map(e, tn, 2);
+    const CUtensorMap* tex = dev_act_map(e, tn, 3);
+    FStage emb;
+    memset(&emb, 0, sizeof(emb));
+    emb.type = IT_EMBED;
+    emb.dep = -1;
+    emb.em = EmbedArgs{(const int32_t*)(e->meta_dev + e->off_tok), e->embed, e->norm_attn[0], e->h, e->u,
+                       ssq_at(e, 0, 0), M, e->MP, d};
+    B += Md * 8;
+    int prev = add(emb);
+    const int32_t* ctxh = (const int32_t*)(e->meta_host + e->off_ctx);
+    for (int l = 0; l < L; ++l) {
+        GemmArgs a = base_args(e, M);
+        a.layer = l;
+        a.ssq_in = ssq_at(e, l, 0);
+        a.qbuf = e->qbuf;
+        const int s_qkv = add(gemm_stage(EPI_QKV, e->d_tmaps + l, tu, 3 * d, d, a, prev, Md * 8));
+        FStage at;
+        memset(&at, 0, sizeof(at));
+        at.type = IT_ATTN;
+        at.dep = s_qkv;
+        AttnArgs& aa = at.at;
+        aa.q = e->qbuf; aa.kv_pool = (const bf16_raw_t*)e->kv_pool; aa.out = e->attn_out;
+        aa.part_o = e->attn_o; aa.part_ml = e->attn_ml; aa.counters = e->cnt_attn;
+        aa.ctx = (const int32_t*)(e->meta_dev + e->off_ctx);
+        aa.page_table = (const int32_t*)(e->meta_dev + e->off_pt);
+        aa.pt_stride = e->pt_stride;
+        aa.B = n; aa.G = G; aa.n_heads = e->H; aa.head_dim = e->D; aa.d_model = d; aa.n_layers = L;
+        aa.layer = l; aa.page_tokens = e->cfg.page_tokens; aa.nchunk = nchunk;
+        aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)e->D));
+        B += Md * 6;
+        for (int b = 0; b < n; ++b) {
+            B += (double)(ctxh[b] + G) * d * 4;
+            for (int j = 0; j < G; ++j) FL += 4.0 * (ctxh[b] + j + 1) * d;
+        }
+        const int s_at = add(at);
+        GemmArgs o = base_args(e, M);
+        o.h = e->h; o.g_out = e->norm_mlp[l]; o.u_out = e->u; o.ssq_out = ssq_at(e, l, 1);
+        const int s_o = add(gemm_stage(EPI_RESID, e->d_tmaps + L + l, ta, d, d, o, s_at, Md * 10));
+        GemmArgs gu = base_args(e, M);
+        gu.ssq_in = ssq_at(e, l, 1);
+        gu.act = e->act;
+        const int s_gu = add(gemm_stage(EPI_SWIGLU, e->d_tmaps + 2 * L + l, tu, 2 * F, d, gu, s_o, (double)M * F * 2));
+        GemmArgs dn = base_args(e, M);
+        dn.h = e->h;
+        dn.g_out = (l + 1 < L) ? e->norm_attn[l + 1] : e->norm_final;
+        dn.u_out = e->u;
+        if (l + 1 == exit_layer) {
+            dn.g_out2 = e->norm_final;
+            dn.u_out2 = e->u_exit;
+        }
+        dn.ssq_out = ssq_at(e, l + 1, 0);
+        prev = add(gemm_stage(EPI_RESID, e->d_tmaps + 3 * L + l, tact, d, F, dn, s_gu,
+                              Md * (l + 1 == exit_layer ? 12 : 10)));
+        if (l + 1 == exit_layer) {   // S10-S11 on the exit branch, right after h^(l_e) exists
+            GemmArgs lm = base_args(e, M);
+            lm.ssq_in = ssq_at(e, exit_layer, 0);
+            lm.logits = e->logits_exit;
+            FStage s = gemm_stage(EPI_LOGITS, e->d_tmaps + 4 * L, tex, V, d, lm, prev, (double)M * V * 4);
+            s.exit_ws = 1;
+            const int s_lm = add(s);
+            const int s_stats = add(accept_stage(true, s_lm, true));
+            add(accept_stage(true, s_stats, false));
+        }
+    }
+    GemmArgs lm = base_args(e, M);
+    lm.ssq_in = ssq_at(e, L, 0);
+    lm.logits = e->logits_final;
+    const int s_lm = add(gemm_stage(EPI_LOGITS, e->d_tmaps + 4 * L, tu, V, d, lm, prev, (double)M * V * 4));
+    const int s_stats = add(accept_stage(false, s_lm, true));
+    add(accept_stage(false, s_stats, false));
+    cudaError_t r = fused_build(P, st, e->num_sms, tn, e->D);
+    if (r != cudaSuccess) return r;
+    P->early_host_dev = e->mb_exit_dev;
+    P->early_flag_dev = e->mb_flag_dev;
+    P->seq_dev = (const uint64_t*)(e->meta_dev + e->off_seq);
+    P->n_req = n;
+    *bytes = B;
+    *flops = FL;
+    return cudaSuccess;
+}
+
+static cudaError_t issue_fused(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk,
+                               int* launches) {
+    StepKey key{n, gamma, exit_layer, nchunk};
+    auto it = e->plans.find(key);
+    FusedPlan* P;
+    static std::map<const FusedPlan*, std::pair<double, double>> cost;
+    if (it == e->plans.end()) {
+        P = new FusedPlan();
+        double b = 0, f = 0;
+        cudaError_t r = build_fused_plan(e, n, gamma, exit_layer, nchunk, P, &b, &f);
+        if (r != cudaSuccess) {
+            fused_free(P);
+            delete P;
+            return r;
+        }
+        cost[P] = {b, f};
+        e->plans[key] = P;
+    } else {
+        P = it->second;
+    }
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (e->prof) {
+        cudaEventCreate(&a);
+        cudaEventRecord(a, st);
+    }
+    cudaError_t r = fused_launch(P, st);
+    if (r != cudaSuccess) return r;
+    if (e->prof) {
+        cudaEventCreate(&b);
+        cudaEventRecord(b, st);
+        e->prof->push_back(ProfRec{SV_K_FUSED, -1, st, a, b, cost[P].first, cost[P].second});
+    }
+    r = cudaMemcpyAsync(e->mb_final, e->res_final_dev, (size_t)n * sizeof(sv_exit_result), cudaMemcpyDeviceToHost, st);
+    *launches = 1;
+    return r;
 }
 
 static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk) {

@@ -35,6 +35,7 @@
 #include <cstdio>
 
 #include "common.cuh"
+#include "gemm_epi.cuh"
 #include "kernels.h"
 
 namespace sv {
@@ -42,7 +43,6 @@ namespace sv {
 constexpr int BK = 64;                      // K elements per stage (one 128 B swizzle row)
 constexpr int TM = 128;                     // weight rows per tile (UMMA M)
 constexpr int A_STAGE = TM * BK * 2;        // 16 KB
-constexpr int EPI_CHUNK = 16;               // token columns per epilogue pass
 #ifndef SV_GEMM_CTAS_PER_SM
 #define SV_GEMM_CTAS_PER_SM 2
 #endif
@@ -64,81 +64,14 @@ struct GemmCfg {
     static_assert(EPI_CHUNK * TM * 4 <= STAGES * STAGE, "epilogue tile must fit the ring");
 };
 
+struct GemmCtaSync {
+    __device__ void operator()() const { __syncthreads(); }
+};
+
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const float* sOut, const float* sR, float* sRed,
                                           int tok0, int m0, int n0, int nt) {
-    const int r = threadIdx.x;
-    const int warp = r >> 5, lane = r & 31;
-    if constexpr (EPI == EPI_QKV) {
-        const int d = a.d_model, D = a.head_dim, half = D >> 1;
-        const int sec = n0 / d;                // 0 = q, 1 = k, 2 = v
-        const int col = (n0 % d) + r;
-        const int hd = col / D, i = col % D;
-        const int rp = r - i + ((i + half) % D);
-        for (int j = 0; j < EPI_CHUNK; ++j) {
-            const int tok = tok0 + j;
-            if (tok >= a.M) break;
-            const float rs = sR[tok - m0];
-            float v = sOut[j * TM + r] * rs;
-            const int pos = a.meta.pos[tok];
-            if (sec < 2) {
-                const float vp = sOut[j * TM + rp] * rs;
-                const float2 cs = reinterpret_cast<const float2*>(a.rope_cs)[(size_t)pos * half + (i % half)];
-                v = (i < half) ? (v * cs.x - vp * cs.y) : (v * cs.x + vp * cs.y);
-            }
-            if (sec == 0) {
-                a.qbuf[(size_t)tok * d + col] = v;
-            } else {
-                const int b = a.meta.row_req[tok];
-                const int blk = a.meta.page_table[b * a.meta.pt_stride + pos / a.page_tokens];
-                const int slot = pos % a.page_tokens;
-                const size_t off = (((size_t)blk * a.n_layers + a.layer) * 2 + (sec - 1)) *
-                                       ((size_t)a.n_heads * a.page_tokens * D) +
-                                   ((size_t)hd * a.page_tokens + slot) * D + i;
-                reinterpret_cast<bf16*>(a.kv_pool)[off] = __float2bfloat16_rn(v);
-            }
-        }
-    } else if constexpr (EPI == EPI_RESID) {
-        const int d = a.d_model;
-        const float g = __bfloat162float(reinterpret_cast<const bf16*>(a.g_out)[n0 + r]);
-        const float g2 = a.u_out2 ? __bfloat162float(reinterpret_cast<const bf16*>(a.g_out2)[n0 + r]) : 0.f;
-        for (int j = 0; j < EPI_CHUNK; ++j) {
-            const int tok = tok0 + j;
-            float hv = 0.f;
-            if (tok < a.M) {
-                const size_t idx = (size_t)tok * d + n0 + r;
-                hv = a.h[idx] + sOut[j * TM + r];
-                a.h[idx] = hv;
-                reinterpret_cast<bf16*>(a.u_out)[idx] = __float2bfloat16_rn(hv * g);
-                if (a.u_out2) reinterpret_cast<bf16*>(a.u_out2)[idx] = __float2bfloat16_rn(hv * g2);
-            }
-            const float sq = warp_sum(hv * hv);
-            if (lane == 0) sRed[warp * EPI_CHUNK + j] = sq;
-        }
-        __syncthreads();
-        if (r < EPI_CHUNK && tok0 + r < a.M) {
-            const float s = (sRed[0 * EPI_CHUNK + r] + sRed[1 * EPI_CHUNK + r]) +
-                            (sRed[2 * EPI_CHUNK + r] + sRed[3 * EPI_CHUNK + r]);
-            a.ssq_out[(size_t)nt * a.MP + tok0 + r] = s;
-        }
-    } else if constexpr (EPI == EPI_SWIGLU) {
-        const int rr = r & 63, jh = r >> 6;
-        for (int j = jh * (EPI_CHUNK / 2); j < (jh + 1) * (EPI_CHUNK / 2); ++j) {
-            const int tok = tok0 + j;
-            if (tok >= a.M) break;
-            const float rs = sR[tok - m0];
-            const float g = sOut[j * TM + rr] * rs;
-            const float u = sOut[j * TM + 64 + rr] * rs;
-            const float y = g / (1.0f + expf(-g)) * u;
-            reinterpret_cast<bf16*>(a.act)[(size_t)tok * a.d_ff + nt * 64 + rr] = __float2bfloat16_rn(y);
-        }
-    } else {  // EPI_LOGITS
-        for (int j = 0; j < EPI_CHUNK; ++j) {
-            const int tok = tok0 + j;
-            if (tok >= a.M) break;
-            a.logits[(size_t)tok * a.N + n0 + r] = sOut[j * TM + r] * sR[tok - m0];
-        }
-    }
+    epi_apply<EPI>(a, sOut, sR, sRed, tok0, m0, n0, nt, (int)threadIdx.x, GemmCtaSync{});
 }
 
 template <int TN, int EPI>
@@ -226,24 +159,7 @@ __global__ void __launch_bounds__(128, 1)
     pdl_wait();   // everything below reads data produced by the previous kernel
 
     // rstd of the RMSNorm folded into this GEMM (fixed summation order)
-    for (int t = threadIdx.x; t < TN; t += blockDim.x) {
-        const int tok = m0 + t;
-        float rs = 1.0f;
-        if (a.ssq_in && tok < a.M) {
-            float s = 0.f;
-            int k = 0;
-            for (; k + 8 <= a.ssq_tiles; k += 8) {   // 8 loads in flight, summed in tile order
-                float v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = a.ssq_in[(size_t)(k + u) * a.MP + tok];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) s += v[u];
-            }
-            for (; k < a.ssq_tiles; ++k) s += a.ssq_in[(size_t)k * a.MP + tok];
-            rs = 1.0f / sqrtf(s * a.inv_d + a.eps);
-        }
-        sR[t] = rs;
-    }
+    epi_rstd(a, sR, m0, TN, threadIdx.x, blockDim.x);
 
     mbar_wait(done, 0);
     tc_fence_after();

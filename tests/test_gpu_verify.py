@@ -20,17 +20,17 @@ pytestmark = pytest.mark.gpu
 LOGIT_TOL = 2e-2
 
 
-def _setup(mc, B, max_gamma=8, use_graphs=True):
+def _setup(mc, B, max_gamma=8, use_graphs=True, fused=None):
     from paper_2505_21594_b200 import sv
     W = sv.Weights(mc, seed=1)
-    eng = sv.Engine(mc, W, max_batch=B, max_gamma=max_gamma, use_graphs=use_graphs)
+    eng = sv.Engine(mc, W, max_batch=B, max_gamma=max_gamma, use_graphs=use_graphs, fused=fused)
     return sv, W, eng
 
 
-def _run_rounds(mc, B, gamma, ctx, exit_layer, greedy, rounds, use_graphs=True, model=None):
+def _run_rounds(mc, B, gamma, ctx, exit_layer, greedy, rounds, use_graphs=True, model=None, fused=None):
     """Run `rounds` verify steps on B sessions through libsv and the oracle in
     lockstep (each side keeps its own cache); returns the tally and errors."""
-    sv, W, eng = _setup(mc, B, use_graphs=use_graphs)
+    sv, W, eng = _setup(mc, B, use_graphs=use_graphs, fused=fused)
     model = model or om.Model(mc, seed=1)
     gs, os_ = [], []
     for b in range(B):
@@ -75,20 +75,22 @@ def _run_rounds(mc, B, gamma, ctx, exit_layer, greedy, rounds, use_graphs=True, 
     return tally_f, tally_e, np.array(errs)
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "per_op"])
 @pytest.mark.parametrize("greedy", [True, False], ids=["greedy", "stochastic"])
 @pytest.mark.parametrize("ctx", [64, 59])
-def test_tiny_end_to_end(svlib, greedy, ctx):
+def test_tiny_end_to_end(svlib, greedy, ctx, fused):
     """configs[0]: 2 layers, d=128, 4 heads, V=512, ctx 64 (or 59 = 64 - G), gamma=4,
-    batch 1, early exit at layer 1."""
-    tf, te, errs = _run_rounds(tiny(), 1, 4, ctx, 1, greedy, rounds=4)
+    batch 1, early exit at layer 1; both engines (fused persistent step, per-op kernels)."""
+    tf, te, errs = _run_rounds(tiny(), 1, 4, ctx, 1, greedy, rounds=4, fused=fused)
     print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
     assert errs.max() < LOGIT_TOL
     assert not tf.hard_mismatch and not te.hard_mismatch
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "per_op"])
 @pytest.mark.parametrize("gamma", [1, 3, 8])
-def test_tiny_batched_gamma_sweep(svlib, gamma):
-    tf, te, errs = _run_rounds(tiny(), 5, gamma, 37, 2, False, rounds=2)
+def test_tiny_batched_gamma_sweep(svlib, gamma, fused):
+    tf, te, errs = _run_rounds(tiny(), 5, gamma, 37, 2, False, rounds=2, fused=fused)
     print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
     assert errs.max() < LOGIT_TOL
     assert not tf.hard_mismatch and not te.hard_mismatch
@@ -216,11 +218,12 @@ def test_host_probs_equal_device_probs(svlib):
     eng.close()
 
 
-def test_7b_width_two_layers(svlib):
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "per_op"])
+def test_7b_width_two_layers(svlib, fused):
     """Llama2-7B layer shapes (d=4096, 32 heads, F=11008, V=32000) with 2 layers,
     batch 2, ctx 200: logits and decisions vs the fp64 oracle."""
     mc = ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=512)
-    tf, te, errs = _run_rounds(mc, 2, 4, 200, 1, False, rounds=2)
+    tf, te, errs = _run_rounds(mc, 2, 4, 200, 1, False, rounds=2, fused=fused)
     print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
     assert errs.max() < LOGIT_TOL
     assert not tf.hard_mismatch and not te.hard_mismatch
