@@ -9,7 +9,7 @@
 #ifndef SV_SPIN_LIMIT
 // bounded spin for every device-side wait: a protocol bug traps (launch error)
 // instead of hanging the GPU
-#define SV_SPIN_LIMIT (1u << 30)
+#define SV_SPIN_LIMIT (1u << 26)
 #endif
 
 namespace sv {
