@@ -818,26 +818,36 @@ static cudaError_t build_fused_plan(sv_engine* e, int n, int gamma, int exit_lay
     return cudaSuccess;
 }
 
-static cudaError_t issue_fused(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk,
-                               int* launches) {
+static std::map<const FusedPlan*, std::pair<double, double>> g_plan_cost;
+
+// Builds (once per key, outside any stream capture: it allocates and uploads).
+static cudaError_t ensure_plan(sv_engine* e, int n, int gamma, int exit_layer, int nchunk, FusedPlan** out) {
     StepKey key{n, gamma, exit_layer, nchunk};
     auto it = e->plans.find(key);
-    FusedPlan* P;
-    static std::map<const FusedPlan*, std::pair<double, double>> cost;
-    if (it == e->plans.end()) {
-        P = new FusedPlan();
-        double b = 0, f = 0;
-        cudaError_t r = build_fused_plan(e, n, gamma, exit_layer, nchunk, P, &b, &f);
-        if (r != cudaSuccess) {
-            fused_free(P);
-            delete P;
-            return r;
-        }
-        cost[P] = {b, f};
-        e->plans[key] = P;
-    } else {
-        P = it->second;
+    if (it != e->plans.end()) {
+        *out = it->second;
+        return cudaSuccess;
     }
+    FusedPlan* P = new FusedPlan();
+    double b = 0, f = 0;
+    cudaError_t r = build_fused_plan(e, n, gamma, exit_layer, nchunk, P, &b, &f);
+    if (r != cudaSuccess) {
+        fused_free(P);
+        delete P;
+        return r;
+    }
+    g_plan_cost[P] = {b, f};
+    e->plans[key] = P;
+    *out = P;
+    return cudaSuccess;
+}
+
+static cudaError_t issue_fused(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk,
+                               int* launches) {
+    FusedPlan* P = nullptr;
+    cudaError_t r0 = ensure_plan(e, n, gamma, exit_layer, nchunk, &P);
+    if (r0 != cudaSuccess) return r0;
+    auto& cost = g_plan_cost;
     cudaEvent_t a = nullptr, b = nullptr;
     if (e->prof) {
         cudaEventCreate(&a);
@@ -866,6 +876,10 @@ static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, int e
     StepKey key{n, gamma, exit_layer, nchunk};
     auto it = e->graphs.find(key);
     if (it == e->graphs.end()) {
+        if (e->opts.fused) {
+            FusedPlan* P = nullptr;
+            CK(ensure_plan(e, n, gamma, exit_layer, nchunk, &P));
+        }
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(e->s_cap, cudaStreamCaptureModeThreadLocal));
         cudaError_t r = issue_step(e, e->s_cap, n, gamma, exit_layer, nchunk, &nl);
