@@ -167,6 +167,9 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                 if (st == sat) return true;
                 const FStage& S = f.stages[st];
                 if (S.dep < 0 || ld_acquire(&f.cnt[S.dep]) >= S.dep_target) {
+                    // once per newly satisfied dependency: make the producers' generic
+                    // stores (acquired above) visible to this thread's async-proxy reads
+                    fence_proxy_async_global();
                     sat = st;
                     return true;
                 }
@@ -176,7 +179,6 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                 while (qh != qt) {
                     const int k = qh % C::STAGES;
                     if (!dep_ok(qst[k])) break;
-                    fence_proxy_async_global();
                     tma_load_2d(f.stages[qst[k]].tmB, sB + qs[k] * C::B_STAGE, &full[qs[k]], qkb[k] * F_BK, qm0[k],
                                 pol_x);
                     ++qh;
