@@ -210,6 +210,7 @@ struct sv_engine {
     // fused persistent step: device-resident tensor maps and per-key plans
     CUtensorMap* d_tmaps = nullptr;             // [4L+1 weights][5 tile sizes x 4 activation maps]
     std::map<StepKey, FusedPlan*> plans;
+    FusedPlan* last_plan = nullptr;
     // tensor maps
     std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;
     CUtensorMap tm_lm;
@@ -847,6 +848,7 @@ static cudaError_t issue_fused(sv_engine* e, cudaStream_t st, int n, int gamma, 
     FusedPlan* P = nullptr;
     cudaError_t r0 = ensure_plan(e, n, gamma, exit_layer, nchunk, &P);
     if (r0 != cudaSuccess) return r0;
+    e->last_plan = P;
     auto& cost = g_plan_cost;
     cudaEvent_t a = nullptr, b = nullptr;
     if (e->prof) {
@@ -1070,6 +1072,7 @@ extern "C" sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us) {
         }
     }
     t->final_done = true;
+    if (e->opts.fused && e->last_plan && e->last_plan->d_trace) fused_dump_trace(e->last_plan, getenv("SV_TRACE"));
     e->inflight = nullptr;
     return SV_OK;
 }

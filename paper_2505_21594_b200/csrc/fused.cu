@@ -23,6 +23,8 @@
 // in stage order, so the persistent grid (co-resident, cooperative launch) cannot
 // deadlock; all spins are bounded (trap).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -76,7 +78,14 @@ struct FArgs {
     sv_exit_result* early_host;
     uint64_t* early_flag;
     const uint64_t* seq;
+    unsigned long long* trace;   // optional timeline [item][4] (globaltimer ns), nullptr = off
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
@@ -160,7 +169,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
         if (lane == 0) {
             // ------------------------------------------------ TMA producer
             const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-            int qs[C::STAGES], qst[C::STAGES], qkb[C::STAGES], qm0[C::STAGES];
+            int qs[C::STAGES], qst[C::STAGES], qkb[C::STAGES], qm0[C::STAGES], qit[C::STAGES];
             int qh = 0, qt = 0, a_cnt = 0, sat = -1;
             uint32_t spins = 0;
             auto dep_ok = [&](int st) -> bool {
@@ -181,6 +190,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                     if (!dep_ok(qst[k])) break;
                     tma_load_2d(f.stages[qst[k]].tmB, sB + qs[k] * C::B_STAGE, &full[qs[k]], qkb[k] * F_BK, qm0[k],
                                 pol_x);
+                    if (f.trace && qit[k] >= 0) f.trace[(size_t)qit[k] * 4 + 1] = gtimer();
                     ++qh;
                 }
             };
@@ -201,8 +211,10 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                     }
                     mbar_arrive_expect_tx(&full[s], C::STAGE);
                     tma_load_2d(S.tmA, sA + s * F_A_STAGE, &full[s], kb * F_BK, n0, pol_w);
+                    if (f.trace && kb == I.kb0) f.trace[(size_t)it * 4 + 0] = gtimer();
                     const int k = qt % C::STAGES;
                     qs[k] = s; qst[k] = I.stage; qkb[k] = kb; qm0[k] = m0;
+                    qit[k] = (kb == I.kb0) ? it : -1;
                     ++qt;
                     ++a_cnt;
                     service();
@@ -257,6 +269,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                 mbar_wait(&tfull[buf], (seg >> 1) & 1);
                 tc_fence_after();
                 wait_stage(f, S, wt, wsync);
+                if (f.trace && wt == 0) f.trace[(size_t)it * 4 + 2] = gtimer();
                 const GemmArgs& g = S.g;
                 const int nt = I.tile / S.nt_m, n0 = nt * F_TM, m0 = (I.tile % S.nt_m) * TN;
                 const uint32_t tb = tmem + tlane + buf * C::TBUF;
@@ -331,6 +344,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                 }
             } else if (I.type == IT_ATTN) {
                 wait_stage(f, S, wt, wsync);
+                if (f.trace && wt == 0) f.trace[(size_t)it * 4 + 2] = gtimer();
                 const bool merged = attn_page_body<D>(S.at, I.tile, I.kb0, wt,
                                                       *reinterpret_cast<AttnSmem<D>*>(uni), wsync);
                 if (merged) {
@@ -342,6 +356,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                 wsync();
             } else if (I.type == IT_STATS) {
                 wait_stage(f, S, wt, wsync);
+                if (f.trace && wt == 0) f.trace[(size_t)it * 4 + 2] = gtimer();
                 AcceptSmem& A = *reinterpret_cast<AcceptSmem*>(uni);
                 if (S.ac.req[I.tile / S.ac.G].status_in == 0) row_stats_body<128>(S.ac, I.tile, I.kb0, wt, A, wsync);
                 __threadfence();
@@ -349,6 +364,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                 if (wt == 0) atomicAdd(&f.cnt[I.stage], 1);
             } else if (I.type == IT_ACCEPT) {
                 wait_stage(f, S, wt, wsync);
+                if (f.trace && wt == 0) f.trace[(size_t)it * 4 + 2] = gtimer();
                 AcceptSmem& A = *reinterpret_cast<AcceptSmem*>(uni);
                 const bool fin = accept_body<128>(S.ac, I.tile, I.kb0, wt, A, wsync);
                 if (fin) {
@@ -386,6 +402,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                 wsync();
                 if (wt == 0) atomicAdd(&f.cnt[I.stage], 1);
             }
+            if (f.trace && wt == 0) f.trace[(size_t)it * 4 + 3] = gtimer();
         }
     }
     tc_fence_before();
@@ -442,6 +459,7 @@ cudaError_t fused_launch(const FusedPlan* p, cudaStream_t st) {
     a.early_host = p->early_host_dev;
     a.early_flag = p->early_flag_dev;
     a.seq = p->seq_dev;
+    a.trace = p->d_trace;
     switch (p->tile_n) {
         case 16: return launch_t<16>(a, p->head_dim, p->num_ctas, st);
         case 32: return launch_t<32>(a, p->head_dim, p->num_ctas, st);
@@ -573,6 +591,13 @@ cudaError_t fused_build(FusedPlan* P, std::vector<FStage>& stages, int num_ctas,
     FB_ALLOC(P->ws_exit, sizeof(float) * 2 * num_ctas * tile_n * 128);
 #undef FB_ALLOC
     P->d_tile_cnt = P->d_cnt + NS;
+    P->h_items = items;
+    P->h_start = start;
+    if (getenv("SV_TRACE")) {
+        if ((e = cudaMalloc((void**)&P->d_trace, sizeof(unsigned long long) * 4 * std::max<size_t>(1, items.size()))))
+            return e;
+        cudaMemset(P->d_trace, 0, sizeof(unsigned long long) * 4 * std::max<size_t>(1, items.size()));
+    }
     if ((e = cudaMemcpy(P->d_stages, stages.data(), sizeof(FStage) * NS, cudaMemcpyHostToDevice))) return e;
     if (!items.empty() &&
         (e = cudaMemcpy(P->d_items, items.data(), sizeof(FItem) * items.size(), cudaMemcpyHostToDevice)))
@@ -584,8 +609,26 @@ cudaError_t fused_build(FusedPlan* P, std::vector<FStage>& stages, int num_ctas,
     return cudaSuccess;
 }
 
+// Timeline of the last step (SV_TRACE=<path>): one CSV row per work item.
+void fused_dump_trace(const FusedPlan* p, const char* path) {
+    if (!p->d_trace || !path) return;
+    std::vector<unsigned long long> t(4 * p->h_items.size());
+    if (cudaMemcpy(t.data(), p->d_trace, t.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    FILE* fp = fopen(path, "w");
+    if (!fp) return;
+    fprintf(fp, "cta,idx,type,stage,tile,kb0,kb1,nsegs,t_a,t_b,t_work,t_end\n");
+    for (int c = 0; c < p->num_ctas; ++c)
+        for (int i = p->h_start[c]; i < p->h_start[c + 1]; ++i) {
+            const FItem& it = p->h_items[i];
+            fprintf(fp, "%d,%d,%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu\n", c, i, it.type, it.stage, it.tile, it.kb0,
+                    it.kb1, it.nsegs, t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]);
+        }
+    fclose(fp);
+}
+
 void fused_free(FusedPlan* p) {
-    void* ptrs[] = {p->d_stages, p->d_items, p->d_item_start, p->d_seg_slots, p->d_cnt, p->ws_main, p->ws_exit};
+    void* ptrs[] = {p->d_stages, p->d_items, p->d_item_start, p->d_seg_slots, p->d_cnt, p->ws_main, p->ws_exit,
+                    p->d_trace};
     for (void* q : ptrs)
         if (q) cudaFree(q);
 }

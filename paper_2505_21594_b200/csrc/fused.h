@@ -49,6 +49,9 @@ struct FusedPlan {
     const uint64_t* seq_dev = nullptr;
     int exit_stage_accept = -1, n_req = 0;
     int n_items = 0;
+    unsigned long long* d_trace = nullptr;      // [n_items][4] timeline (SV_TRACE), else nullptr
+    std::vector<FItem> h_items;                 // host copy of the item list (for trace dumps)
+    std::vector<int> h_start;
 };
 
 // Builds the item lists (stream-K split of every GEMM over num_ctas CTAs, attention
@@ -56,5 +59,6 @@ struct FusedPlan {
 cudaError_t fused_build(FusedPlan* plan, std::vector<FStage>& stages, int num_ctas, int tile_n, int head_dim);
 cudaError_t fused_launch(const FusedPlan* plan, cudaStream_t st);
 void fused_free(FusedPlan* plan);
+void fused_dump_trace(const FusedPlan* plan, const char* path);
 
 }  // namespace sv
