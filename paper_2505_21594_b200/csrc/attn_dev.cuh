@@ -37,13 +37,13 @@ __device__ bool attn_page_body(const AttnArgs& a, int bh, int c, int tid, AttnSm
     const int warp = tid >> 5, lane = tid & 31;
     const int b = bh / a.n_heads, h = bh % a.n_heads;
     const int G = a.G;
-    const int ctx = a.ctx[b];
+    const int ctx = a.ctx[b];                          // both loads issued together
+    const int blk = a.page_table[b * a.pt_stride + c];  // (in bounds; unused if c is past the end)
     const int T = ctx + G;
     const int nch_b = (T + KPAGE - 1) / KPAGE;
     if (c >= nch_b) return false;
     const int k0 = c * KPAGE;
     const int nk = min(KPAGE, T - k0);
-    const int blk = a.page_table[b * a.pt_stride + c];
     const size_t plane = (size_t)a.n_heads * a.page_tokens * D;
     const bf16* Kp = reinterpret_cast<const bf16*>(a.kv_pool) +
                      (((size_t)blk * a.n_layers + a.layer) * 2 + 0) * plane + (size_t)h * a.page_tokens * D;
@@ -89,19 +89,21 @@ __device__ bool attn_page_body(const AttnArgs& a, int bh, int c, int tid, AttnSm
         if (key < nk && k0 + key <= ctx + j) {
             const bf16* kr = &S.sK[key * KST];
             const float* qr = &S.sQ[j * D];
-            float acc = 0.f;
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};       // 4 independent chains (ILP)
 #pragma unroll
             for (int dd = 0; dd < D; dd += 8) {
                 const uint4 kv = *reinterpret_cast<const uint4*>(kr + dd);
+                const float4 q0 = *reinterpret_cast<const float4*>(qr + dd);
+                const float4 q1 = *reinterpret_cast<const float4*>(qr + dd + 4);
                 const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv);
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float2 kf = __bfloat1622float2(k2[t]);
-                    acc = fmaf(qr[dd + 2 * t], kf.x, acc);
-                    acc = fmaf(qr[dd + 2 * t + 1], kf.y, acc);
-                }
+                const float2 f0 = __bfloat1622float2(k2[0]), f1 = __bfloat1622float2(k2[1]);
+                const float2 f2 = __bfloat1622float2(k2[2]), f3 = __bfloat1622float2(k2[3]);
+                acc[0] = fmaf(q0.x, f0.x, fmaf(q0.y, f0.y, acc[0]));
+                acc[1] = fmaf(q0.z, f1.x, fmaf(q0.w, f1.y, acc[1]));
+                acc[2] = fmaf(q1.x, f2.x, fmaf(q1.y, f2.y, acc[2]));
+                acc[3] = fmaf(q1.z, f3.x, fmaf(q1.w, f3.y, acc[3]));
             }
-            s = acc;
+            s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
         }
         S.sS[j * KPAGE + key] = s;
     }
@@ -126,9 +128,15 @@ __device__ bool attn_page_body(const AttnArgs& a, int bh, int c, int tid, AttnSm
     const int dd = tid % D, jg = tid / D;
     const size_t pbase = ((size_t)bh * a.nchunk + c) * G;
     for (int j = jg; j < G; j += JG) {
-        float o = 0.f;
-        for (int key = 0; key < nk; ++key) o = fmaf(S.sS[j * KPAGE + key], __bfloat162float(S.sV[key * D + dd]), o);
-        a.part_o[(pbase + j) * D + dd] = o;
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+        int key = 0;
+        for (; key + 4 <= nk; key += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                o[u] = fmaf(S.sS[j * KPAGE + key + u], __bfloat162float(S.sV[(key + u) * D + dd]), o[u]);
+        }
+        for (; key < nk; ++key) o[0] = fmaf(S.sS[j * KPAGE + key], __bfloat162float(S.sV[key * D + dd]), o[0]);
+        a.part_o[(pbase + j) * D + dd] = (o[0] + o[1]) + (o[2] + o[3]);
     }
     if (tid < G) {
         a.part_ml[(pbase + tid) * 2 + 0] = S.sM[tid];

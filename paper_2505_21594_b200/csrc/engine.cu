@@ -989,7 +989,7 @@ extern "C" sv_status sv_verify_submit(sv_engine* e, const sv_verify_req* reqs, i
     CK(cudaEventCreateWithFlags(&t->ev_done, cudaEventDisableTiming));
     if (t->has_gpu) {
         int nchunk = (max_len + 63) / 64;
-        nchunk = std::min(e->max_nchunk, (nchunk + 3) / 4 * 4);
+        nchunk = std::min(e->max_nchunk, nchunk);   // exact: no empty attention work items
         sv_status s = run_step(e, st, nb, gamma, exit_layer, nchunk);
         if (s) {
             e->poisoned = true;

@@ -58,9 +58,11 @@ struct FCfg {
     static constexpr int U3 = (int)sizeof(AcceptSmem);
     static constexpr int UNION = ((U1 > U2 ? (U1 > U3 ? U1 : U3) : (U2 > U3 ? U2 : U3)) + 127) / 128 * 128;
     static constexpr int BAR = 512;
-    static constexpr int STAGES_RAW = (F_SMEM_MAX - 1024 - UNION - BAR) / STAGE;
+    static constexpr int SCACHE = 1024;      // per-item copy of the stage descriptor
+    static constexpr int STAGES_RAW = (F_SMEM_MAX - 1024 - UNION - BAR - SCACHE) / STAGE;
     static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
-    static constexpr int SMEM = 1024 + STAGES * STAGE + UNION + BAR;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + UNION + BAR + SCACHE;
+    static_assert(sizeof(FStage) <= SCACHE && sizeof(FStage) % 16 == 0, "stage descriptor cache");
     static constexpr int TBUF = TN < 32 ? 32 : TN;                 // TMEM columns per accumulator
     static constexpr int TCOLS = 2 * TBUF <= 32 ? 32 : (2 * TBUF <= 64 ? 64 : (2 * TBUF <= 128 ? 128 : (2 * TBUF <= 256 ? 256 : 512)));
     static_assert(STAGES >= 2, "ring too shallow");
@@ -131,6 +133,59 @@ __device__ __forceinline__ void epi_dispatch(int epi, const GemmArgs& g, const f
     }
 }
 
+// rstd[t] = 1/sqrt(sum_k ssq[k][m0+t] / d + eps) with every load of the step in
+// flight at once: for TN <= 16, 8 groups x 16 tokens, each group sums a contiguous
+// run of tiles in order, then the 8 group sums are added in order (fixed tree).
+template <int TN, class Sync>
+__device__ __forceinline__ void fused_rstd(const GemmArgs& g, float* sR, float* scratch, int m0, int wt, Sync sync) {
+    if (!g.ssq_in) {
+        for (int t = wt; t < TN; t += 128) sR[t] = 1.0f;
+        sync();
+        return;
+    }
+    if constexpr (TN <= 16) {
+        const int grp = wt >> 4, t = wt & 15, tok = m0 + t;
+        const int per = (g.ssq_tiles + 7) / 8, k0 = grp * per;
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = k0 + u;
+            v[u] = (u < per && k < g.ssq_tiles && tok < g.M) ? __ldcg(&g.ssq_in[(size_t)k * g.MP + tok]) : 0.f;
+        }
+        float s = 0.f;
+        for (int u = 0; u < per && u < 8; ++u) s += v[u];
+        for (int k = k0 + 8; k < k0 + per && k < g.ssq_tiles; ++k)       // (d > 8192 only)
+            s += (tok < g.M) ? __ldcg(&g.ssq_in[(size_t)k * g.MP + tok]) : 0.f;
+        scratch[grp * 16 + t] = s;
+        sync();
+        if (wt < 16) {
+            float a = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a += scratch[q * 16 + wt];
+            sR[wt] = 1.0f / sqrtf(a * g.inv_d + g.eps);
+        }
+        sync();
+    } else {
+        for (int t = wt; t < TN; t += 128) {
+            const int tok = m0 + t;
+            float s = 0.f;
+            if (tok < g.M) {
+                int k = 0;
+                for (; k + 16 <= g.ssq_tiles; k += 16) {
+                    float v[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) v[u] = __ldcg(&g.ssq_in[(size_t)(k + u) * g.MP + tok]);
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) s += v[u];
+                }
+                for (; k < g.ssq_tiles; ++k) s += __ldcg(&g.ssq_in[(size_t)k * g.MP + tok]);
+            }
+            sR[t] = 1.0f / sqrtf(s * g.inv_d + g.eps);
+        }
+        sync();
+    }
+}
+
 template <int TN, int D>
 __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_constant__ FArgs f) {
     using C = FCfg<TN, D>;
@@ -144,6 +199,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    FStage* sStage = reinterpret_cast<FStage*>(uni + C::UNION + C::BAR);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int beg = f.item_start[blockIdx.x], end = f.item_start[blockIdx.x + 1];
@@ -260,10 +316,18 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
         const uint32_t tlane = static_cast<uint32_t>((warp & 3) * 32) << 16;
         WorkerSync wsync;
         EpiSmem<TN>& E = *reinterpret_cast<EpiSmem<TN>*>(uni);
-        int seg = 0;
+        int seg = 0, cached = -1;
         for (int it = beg; it < end; ++it) {
             const FItem I = f.items[it];
-            const FStage& S = f.stages[I.stage];
+            if (I.stage != cached) {   // one coalesced copy of the descriptor per stage change
+                wsync();
+                const uint4* src = reinterpret_cast<const uint4*>(f.stages + I.stage);
+                for (int i = wt; i < (int)(sizeof(FStage) / 16); i += 128)
+                    reinterpret_cast<uint4*>(sStage)[i] = __ldg(src + i);
+                wsync();
+                cached = I.stage;
+            }
+            const FStage& S = *sStage;
             if (I.type == IT_GEMM) {
                 const int buf = seg & 1;
                 mbar_wait(&tfull[buf], (seg >> 1) & 1);
@@ -274,7 +338,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                 const int nt = I.tile / S.nt_m, n0 = nt * F_TM, m0 = (I.tile % S.nt_m) * TN;
                 const uint32_t tb = tmem + tlane + buf * C::TBUF;
                 if (I.nsegs == 1) {
-                    epi_rstd(g, E.sR, m0, TN, wt, 128);
+                    fused_rstd<TN>(g, E.sR, E.sOut, m0, wt, wsync);
                     for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
                         if (m0 + c0 >= g.M) break;
                         uint32_t r[16];
@@ -310,7 +374,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                     wsync();
                     if (E.flag) {
                         __threadfence();
-                        epi_rstd(g, E.sR, m0, TN, wt, 128);
+                        fused_rstd<TN>(g, E.sR, E.sOut, m0, wt, wsync);
                         const float* wsb = S.exit_ws ? f.ws_exit : f.ws_main;
                         for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
                             if (m0 + c0 >= g.M) break;
@@ -318,14 +382,23 @@ __global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_c
                             float acc[EPI_CHUNK];
 #pragma unroll
                             for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = 0.f;
-                            for (int s = 0; s < I.nsegs; ++s) {   // k order; 16 loads in flight
-                                const float* p = wsb + (size_t)f.seg_slots[I.seg_first + s] * TN * F_TM +
-                                                 (size_t)c0 * F_TM + row;
-                                float v[EPI_CHUNK];
+                            for (int s0 = 0; s0 < I.nsegs; s0 += 4) {   // k order; 4 segments in flight
+                                float v[4][EPI_CHUNK];
 #pragma unroll
-                                for (int j = 0; j < EPI_CHUNK; ++j) v[j] = (j < nv) ? __ldcg(p + j * F_TM) : 0.f;
+                                for (int u = 0; u < 4; ++u) {
+                                    const bool ok = s0 + u < I.nsegs;
+                                    const float* p = wsb +
+                                                     (size_t)(ok ? f.seg_slots[I.seg_first + s0 + u] : 0) * TN * F_TM +
+                                                     (size_t)c0 * F_TM + row;
 #pragma unroll
-                                for (int j = 0; j < EPI_CHUNK; ++j) acc[j] += v[j];
+                                    for (int j = 0; j < EPI_CHUNK; ++j)
+                                        v[u][j] = (ok && j < nv) ? __ldcg(p + j * F_TM) : 0.f;
+                                }
+#pragma unroll
+                                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                                    for (int j = 0; j < EPI_CHUNK; ++j)
+                                        if (s0 + u < I.nsegs) acc[j] += v[u][j];
                             }
                             wsync();
 #pragma unroll

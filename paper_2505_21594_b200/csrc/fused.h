@@ -11,7 +11,7 @@ enum FItemType { IT_EMBED = 1, IT_GEMM = 2, IT_ATTN = 3, IT_STATS = 4, IT_ACCEPT
 // One stage of the step (an op whose work items may run on any CTA).  Items of
 // a stage may start their dependent part once stage `dep` has completed
 // (cnt[dep] == target[dep]); every stage depends only on earlier stages.
-struct FStage {
+struct alignas(16) FStage {
     int type, dep, dep_target, target;
     int epi, nt_n, nt_m, kblocks, exit_ws, is_exit;
     int tile_base;                 // first per-tile arrival counter of this GEMM
