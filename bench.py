@@ -309,7 +309,7 @@ def run_ours(args):
     gamma, exit_layer = args.gamma, args.exit_layer
     mc = llama2_7b()
     W = sv.Weights(mc, seed=1, device=local)
-    blocks_per = (ctx + gamma + 1 + 63) // 64 + 1
+    blocks_per = (ctx + gamma + 1 + 63) // 64
     eng = sv.Engine(mc, W, max_batch=per, max_gamma=gamma, kv_blocks=per * blocks_per, device=local)
     sessions = []
     for rid in shard(total, world, rank):          # contiguous shard of the request ids
@@ -319,8 +319,9 @@ def run_ours(args):
     pend = prefix_tokens(3 + rank, per, mc.vocab)
     rounds = Rounds()
     # N_SETS independent calibrated draft sets per request; step i verifies set i % N_SETS
+    n_sets = N_SETS if per <= 16 else 2
     sets = [build_calibrated_drafts(sv, eng, sessions, pend, ctx, gamma, args.alpha, mc.vocab,
-                                    7 + 1000 * rank + k, rounds) for k in range(N_SETS)]
+                                    7 + 1000 * rank + k, rounds) for k in range(n_sets)]
     xs = [x for x, _ in sets]
     q_dev = [torch.from_numpy(q).cuda() for _, q in sets]
     q_host = [torch.from_numpy(q).pin_memory().numpy() for _, q in sets]
@@ -328,7 +329,7 @@ def run_ours(args):
     counter = [0]
 
     def step(host_probs=False):
-        k = counter[0] % N_SETS
+        k = counter[0] % n_sets
         counter[0] += 1
         x = xs[k]
         for s in sessions:
@@ -455,6 +456,7 @@ def run_ours(args):
                                    f"{per} request(s)/GPU, ctx {ctx}, gamma {gamma}, early exit at layer "
                                    f"{exit_layer}, stochastic acceptance, alpha {args.alpha}",
                        "global_batch": total, "seq_len": ctx, "gamma": gamma, "exit_layer": exit_layer,
+                       "engine": "fused persistent step kernel" if eng.fused else "per-op kernels + CUDA graph + PDL",
                        "parallelism": f"requests sharded over {world} GPU(s), weights replicated",
                        "l2": "inputs larger than L2 (13.5 GB of weights streamed per step)"},
             "tokens_per_step": round(tot_tokens / (args.steps * total), 4),

@@ -311,7 +311,7 @@ class Engine:
             kv_blocks = max_batch * ((mc.max_ctx + mc.page_tokens - 1) // mc.page_tokens + 1)
         self.kv_pool = torch.empty(blk * kv_blocks, dtype=torch.uint8, device=f"cuda:{device}")
         if fused is None:
-            fused = os.environ.get("SV_FUSED", "1") != "0"
+            fused = os.environ.get("SV_FUSED", "0") == "1"
         opts = sv_engine_opts(max_batch, max_gamma, 1 if use_graphs else 0, 1 if fused else 0)
         self.fused = bool(fused)
         h = C.c_void_p()

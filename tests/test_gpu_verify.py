@@ -96,6 +96,17 @@ def test_tiny_batched_gamma_sweep(svlib, gamma, fused):
     assert not tf.hard_mismatch and not te.hard_mismatch
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "per_op"])
+def test_tiny_large_batch(svlib, fused):
+    """B = 60 requests (M = 300 query rows): the 256-token GEMM tile with two token
+    tiles, the batched attention grid and 60 acceptance instances (configs[3]-style
+    batching at the tiny shape)."""
+    tf, te, errs = _run_rounds(tiny(), 60, 4, 40, 1, False, rounds=2, fused=fused)
+    print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
+    assert errs.max() < LOGIT_TOL
+    assert not tf.hard_mismatch and not te.hard_mismatch
+
+
 def test_tiny_no_graphs_matches_graphs(svlib):
     """Graph replay and direct launches produce bitwise-identical results."""
     mc = tiny()
