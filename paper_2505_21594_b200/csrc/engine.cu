@@ -629,7 +629,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             aa.B = n; aa.G = G; aa.n_heads = e->H; aa.head_dim = e->D; aa.d_model = d; aa.n_layers = L;
             aa.layer = l; aa.page_tokens = e->cfg.page_tokens; aa.nchunk = nchunk;
             aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)e->D));
-            LAUNCH(SV_K_ATTN, l, st, attn_bytes, attn_flops, attn_launch(aa, st));
+            LAUNCH(SV_K_ATTN, l, st, attn_bytes, attn_flops,
+                   attn2_launch(aa, attn2_splits(n, e->H, nchunk, e->num_sms), st));
         }
         {   // O projection + residual
             GemmArgs a = base_args(e, M);

@@ -80,6 +80,9 @@ struct AttnArgs {
     float scale_log2;     // log2(e) / sqrt(head_dim)
 };
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st);
+// v2: TMA-bulk page ring + online softmax + cluster (DSMEM) split merge
+int attn2_splits(int B, int H, int max_pages, int num_sms);
+cudaError_t attn2_launch(const AttnArgs& a, int splits, cudaStream_t st);
 
 // ----------------------------------------------------------- acceptance (K5)
 struct ReqDev {            // per-request metadata for the acceptance kernels
