@@ -630,7 +630,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             aa.layer = l; aa.page_tokens = e->cfg.page_tokens; aa.nchunk = nchunk;
             aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)e->D));
             LAUNCH(SV_K_ATTN, l, st, attn_bytes, attn_flops,
-                   attn2_launch(aa, attn2_splits(n, e->H, nchunk, e->num_sms), st));
+                   e->D == 128 ? attn3_launch(aa, attn3_splits(n, e->H, nchunk, e->num_sms), st)
+                               : attn_launch(aa, st));
         }
         {   // O projection + residual
             GemmArgs a = base_args(e, M);

@@ -80,9 +80,10 @@ struct AttnArgs {
     float scale_log2;     // log2(e) / sqrt(head_dim)
 };
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st);
-// v2: TMA-bulk page ring + online softmax + cluster (DSMEM) split merge
-int attn2_splits(int B, int H, int max_pages, int num_sms);
-cudaError_t attn2_launch(const AttnArgs& a, int splits, cudaStream_t st);
+// v3 (head_dim 128): mma.sync bf16 tensor-core tiles, per-warp cp.async rings,
+// online softmax in registers, cluster (DSMEM) split merge
+int attn3_splits(int B, int H, int max_pages, int num_sms);
+cudaError_t attn3_launch(const AttnArgs& a, int splits, cudaStream_t st);
 
 // ----------------------------------------------------------- acceptance (K5)
 struct ReqDev {            // per-request metadata for the acceptance kernels

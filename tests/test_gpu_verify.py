@@ -107,15 +107,18 @@ def test_tiny_large_batch(svlib, fused):
     assert not tf.hard_mismatch and not te.hard_mismatch
 
 
-def test_tiny_no_graphs_matches_graphs(svlib):
-    """Graph replay and direct launches produce bitwise-identical results."""
-    mc = tiny()
+@pytest.mark.parametrize("shape", ["tiny", "7b_width"])
+def test_tiny_no_graphs_matches_graphs(svlib, shape):
+    """Graph replay and direct launches produce bitwise-identical results
+    (the 7B-width case covers the tensor-core attention with cluster merges)."""
+    mc = tiny() if shape == "tiny" else ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008,
+                                                  vocab=32000, max_ctx=512)
     res = []
     for ug in (True, False):
         sv, W, eng = _setup(mc, 2, use_graphs=ug)
         ss = [eng.open_session(1 + b, 7 + b) for b in range(2)]
         for b, s in enumerate(ss):
-            s.fill_kv(40, kv_seed=5 + b)
+            s.fill_kv(40 if shape == "tiny" else 300, kv_seed=5 + b)
         x, q = wd.timing_drafts(9, 2, 4, mc.vocab, s=1.1)
         qd = torch.from_numpy(q).cuda()
         t = eng.submit([sv.Request(ss[b], 1, 3, x[b], qd[b]) for b in range(2)], exit_layer=1)
