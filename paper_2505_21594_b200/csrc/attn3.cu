@@ -172,6 +172,16 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
         __syncwarp();
         const uint32_t sk = wring + stage * A3_STAGE, sv = sk + A3_CHB;
         const int kabs0 = (p0 * 64) + ci * A3_CHUNK;
+        const int valid = T - kabs0;                          // rows past the sequence end hold
+        if (valid < A3_CHUNK) {                               // arbitrary bits: zero them (P = 0
+            const int v0 = valid > 0 ? valid : 0;             // times NaN would poison P V)
+            for (int i = lane; i < (A3_CHUNK - v0) * 16; i += 32) {
+                const int row = v0 + (i >> 4), c = i & 15;
+                asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(sk + swz(row, c)), "r"(0) : "memory");
+                asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(sv + swz(row, c)), "r"(0) : "memory");
+            }
+            __syncwarp();
+        }
         // ---- S = Q K^T  (16 x 32)
         float sacc[4][4];
 #pragma unroll

@@ -195,6 +195,36 @@ def test_rollback_bit_exact(svlib):
     eng.close()
 
 
+@pytest.mark.parametrize("shape,fused", [("tiny", False), ("tiny", True), ("7b_width", False)])
+def test_poisoned_kv_tail_is_invisible(svlib, shape, fused):
+    """DESIGN.md R22 (iii): KV slots at or beyond the cached length hold arbitrary
+    bits (here all-NaN bf16 0xFFFF) without changing a step: results and logits are
+    bitwise equal to a run on a zeroed pool."""
+    mc = tiny() if shape == "tiny" else ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008,
+                                                  vocab=32000, max_ctx=512)
+    from paper_2505_21594_b200 import sv
+    W = sv.Weights(mc, seed=1)
+    outs = []
+    for fill in (0, 255):
+        eng = sv.Engine(mc, W, max_batch=2, max_gamma=8, fused=fused)
+        eng.kv_pool.fill_(fill)
+        ss = [eng.open_session(1 + b, 7 + b) for b in range(2)]
+        for b, s in enumerate(ss):
+            s.fill_kv(37 + 50 * b, kv_seed=5 + b)
+        x, q = wd.timing_drafts(9, 2, 4, mc.vocab, s=1.1)
+        qd = torch.from_numpy(q).cuda()
+        t = eng.submit([sv.Request(ss[b], 1, 3, x[b], qd[b]) for b in range(2)], exit_layer=1)
+        t.wait_early()
+        f = t.wait_final()
+        z = t.logits(1, 4).cpu().numpy()
+        outs.append(([r.asdict() for r in f], z))
+        t.release()
+        eng.close()
+    assert np.isfinite(outs[1][1]).all()
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
 def test_protocol_errors(svlib):
     mc = tiny()
     sv, W, eng = _setup(mc, 2)
