@@ -29,24 +29,43 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
         const int col = (n0 % d) + r;
         const int hd = col / D, i = col % D;
         const int rp = r - i + ((i + half) % D);
+        const int nv = min(EPI_CHUNK, a.M - tok0);
+        // every global load of the chunk is issued before the first store (the loop
+        // below would otherwise serialise one memory round trip per token: the
+        // compiler cannot move loads across the stores of the previous token)
+        int pos[EPI_CHUNK], blk[EPI_CHUNK];
+        float2 cs[EPI_CHUNK];
+#pragma unroll
+        for (int j = 0; j < EPI_CHUNK; ++j) pos[j] = (j < nv) ? a.meta.pos[tok0 + j] : 0;
+        if (sec >= 1) {
+            int req[EPI_CHUNK];
+#pragma unroll
+            for (int j = 0; j < EPI_CHUNK; ++j) req[j] = (j < nv) ? a.meta.row_req[tok0 + j] : 0;
+#pragma unroll
+            for (int j = 0; j < EPI_CHUNK; ++j)
+                blk[j] = (j < nv) ? a.meta.page_table[req[j] * a.meta.pt_stride + pos[j] / a.page_tokens] : 0;
+        }
+        if (sec < 2) {
+#pragma unroll
+            for (int j = 0; j < EPI_CHUNK; ++j)
+                cs[j] = (j < nv) ? reinterpret_cast<const float2*>(a.rope_cs)[(size_t)pos[j] * half + (i % half)]
+                                 : make_float2(1.f, 0.f);
+        }
+#pragma unroll
         for (int j = 0; j < EPI_CHUNK; ++j) {
+            if (j >= nv) continue;
             const int tok = tok0 + j;
-            if (tok >= a.M) break;
             const float rs = sR[tok - m0];
             float v = sOut[j * TM + r] * rs;
-            const int pos = a.meta.pos[tok];
             if (sec < 2) {
                 const float vp = sOut[j * TM + rp] * rs;
-                const float2 cs = reinterpret_cast<const float2*>(a.rope_cs)[(size_t)pos * half + (i % half)];
-                v = (i < half) ? (v * cs.x - vp * cs.y) : (v * cs.x + vp * cs.y);
+                v = (i < half) ? (v * cs[j].x - vp * cs[j].y) : (v * cs[j].x + vp * cs[j].y);
             }
             if (sec == 0) {
                 a.qbuf[(size_t)tok * d + col] = v;
             } else {
-                const int b = a.meta.row_req[tok];
-                const int blk = a.meta.page_table[b * a.meta.pt_stride + pos / a.page_tokens];
-                const int slot = pos % a.page_tokens;
-                const size_t off = (((size_t)blk * a.n_layers + a.layer) * 2 + (sec - 1)) *
+                const int slot = pos[j] % a.page_tokens;
+                const size_t off = (((size_t)blk[j] * a.n_layers + a.layer) * 2 + (sec - 1)) *
                                        ((size_t)a.n_heads * a.page_tokens * D) +
                                    ((size_t)hd * a.page_tokens + slot) * D + i;
                 reinterpret_cast<bf16*>(a.kv_pool)[off] = __float2bfloat16_rn(v);
@@ -56,17 +75,21 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
         const int d = a.d_model;
         const float g = __bfloat162float(reinterpret_cast<const bf16*>(a.g_out)[n0 + r]);
         const float g2 = a.u_out2 ? __bfloat162float(reinterpret_cast<const bf16*>(a.g_out2)[n0 + r]) : 0.f;
+        const int nv = min(EPI_CHUNK, a.M - tok0);
+        float hv[EPI_CHUNK];
+#pragma unroll
+        for (int j = 0; j < EPI_CHUNK; ++j)          // all residual loads in flight first
+            hv[j] = (j < nv) ? __ldcg(&a.h[(size_t)(tok0 + j) * d + n0 + r]) : 0.f;
+#pragma unroll
         for (int j = 0; j < EPI_CHUNK; ++j) {
-            const int tok = tok0 + j;
-            float hv = 0.f;
-            if (tok < a.M) {
-                const size_t idx = (size_t)tok * d + n0 + r;
-                hv = __ldcg(&a.h[idx]) + sOut[j * TM + r];
-                a.h[idx] = hv;
-                reinterpret_cast<bf16*>(a.u_out)[idx] = __float2bfloat16_rn(hv * g);
-                if (a.u_out2) reinterpret_cast<bf16*>(a.u_out2)[idx] = __float2bfloat16_rn(hv * g2);
+            if (j < nv) {
+                const size_t idx = (size_t)(tok0 + j) * d + n0 + r;
+                hv[j] += sOut[j * TM + r];
+                a.h[idx] = hv[j];
+                reinterpret_cast<bf16*>(a.u_out)[idx] = __float2bfloat16_rn(hv[j] * g);
+                if (a.u_out2) reinterpret_cast<bf16*>(a.u_out2)[idx] = __float2bfloat16_rn(hv[j] * g2);
             }
-            const float sq = warp_sum(hv * hv);
+            const float sq = warp_sum(hv[j] * hv[j]);
             if (lane == 0) sRed[warp * EPI_CHUNK + j] = sq;
         }
         sync();
