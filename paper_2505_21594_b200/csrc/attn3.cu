@@ -331,11 +331,12 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
 }
 
 int attn3_splits(int B, int H, int max_pages, int num_sms) {
+    // one CTA (4 warps, ~136 KB smem) per SM and ONE wave: the largest power-of-two
+    // cluster size whose clusters all fit (5-CTA clusters pack badly into the
+    // 16-20-SM GPCs: measured 26 of 32 clusters resident -> two waves)
     const int units = B * H;
-    int s = (num_sms + units - 1) / units;                     // ~1 CTA (4 warps) per SM
-    if (s > 8) s = 8;
-    if (s > max_pages) s = max_pages;
-    if (s < 1) s = 1;
+    int s = 1;
+    while (s < 8 && units * (2 * s) <= (num_sms * 7) / 8 && 2 * s <= max_pages) s *= 2;
     return s;
 }
 

@@ -62,6 +62,7 @@ struct GemmCfg {
     static constexpr int SMEM = 1024 + STAGES * STAGE + AUX;
     static_assert(STAGES >= 2, "pipeline too shallow");
     static_assert(EPI_CHUNK * TM * 4 <= STAGES * STAGE, "epilogue tile must fit the ring");
+    static_assert(TN > 64 || (TN + EPI_CHUNK) * TM * 4 <= STAGES * STAGE, "split partial + epilogue tile");
 };
 
 struct GemmCtaSync {
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(128, 1)
     const int row = warp * 32 + lane;
     const uint32_t tbase = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     const bool direct = (a.splits == 1);
+    float* sPart = reinterpret_cast<float*>(smem);       // split partial [TN][128] (the ring is free)
     for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
         if (m0 + c0 >= a.M) break;                       // CTA-uniform
         uint32_t r[16];
@@ -179,12 +181,8 @@ __global__ void __launch_bounds__(128, 1)
             __syncthreads();
             epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt);
         } else {
-            float* wsp = a.ws + (((size_t)split * NT + nt) * a.MP) * TM;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int tok = m0 + c0 + j;
-                if (tok < a.M) wsp[(size_t)tok * TM + row] = __uint_as_float(r[j]);
-            }
+            for (int j = 0; j < 16; ++j) sPart[(c0 + j) * TM + row] = __uint_as_float(r[j]);
         }
     }
     tc_fence_before();
@@ -192,52 +190,33 @@ __global__ void __launch_bounds__(128, 1)
     if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
     if (direct) return;
 
-    // ---------------- split-K: the last CTA of this tile reduces in split order
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int old = atomicAdd(&a.counters[nt * MT + mt], 1);
-        *s_flag = (old == a.splits - 1);
-    }
-    __syncthreads();
-    if (!*s_flag) return;
-    __threadfence();
-    const size_t sstride = (size_t)NT * a.MP * TM;     // distance between two splits' partials
-    for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
-        if (m0 + c0 >= a.M) break;
-        const int nv = min(EPI_CHUNK, a.M - (m0 + c0));
-        // acc[j] = ((p_0 + p_1) + p_2) + ... in split order; the loads of 4 splits x
-        // all valid tokens are issued before any add (the sum order is unchanged)
-        float acc[EPI_CHUNK];
+    // ---------------- split-K through distributed shared memory: the splits of a
+    // tile are one thread-block cluster (dims 1 x 1 x S, rank = split); rank 0 adds
+    // the partials in rank order (deterministic) and runs the fused epilogue.
+    cluster_sync_all();                                  // every split's partial is in its smem
+    if (split == 0) {
+        float* sO = sPart + TN * TM;
+        for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
+            if (m0 + c0 >= a.M) break;
+            const int nv = min(EPI_CHUNK, a.M - (m0 + c0));
+            float acc[EPI_CHUNK];
 #pragma unroll
-        for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = 0.f;
-        const float* base = a.ws + ((size_t)nt * a.MP + m0 + c0) * TM + row;
-        int s = 0;
-        for (; s + 4 <= a.splits; s += 4) {
-            float v[EPI_CHUNK][4];
+            for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = sPart[(c0 + j) * TM + row];
+            for (int q = 1; q < a.splits; ++q) {
+                float v[EPI_CHUNK];
 #pragma unroll
-            for (int j = 0; j < EPI_CHUNK; ++j)
+                for (int j = 0; j < EPI_CHUNK; ++j) v[j] = (j < nv) ? ld_dsmem_f32(&sPart[(c0 + j) * TM + row], q) : 0.f;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) v[j][u] = (j < nv) ? __ldcg(base + (s + u) * sstride + j * TM) : 0.f;
+                for (int j = 0; j < EPI_CHUNK; ++j) acc[j] += v[j];
+            }
+            __syncthreads();
 #pragma unroll
-            for (int j = 0; j < EPI_CHUNK; ++j)
-#pragma unroll
-                for (int u = 0; u < 4; ++u) acc[j] += v[j][u];
+            for (int j = 0; j < EPI_CHUNK; ++j) sO[j * TM + row] = acc[j];
+            __syncthreads();
+            epi_chunk<EPI>(a, sO, sR, sRed, m0 + c0, m0, n0, nt);
         }
-        for (; s < a.splits; ++s) {
-            float v[EPI_CHUNK];
-#pragma unroll
-            for (int j = 0; j < EPI_CHUNK; ++j) v[j] = (j < nv) ? __ldcg(base + s * sstride + j * TM) : 0.f;
-#pragma unroll
-            for (int j = 0; j < EPI_CHUNK; ++j) acc[j] += v[j];
-        }
-#pragma unroll
-        for (int j = 0; j < EPI_CHUNK; ++j) sOut[j * TM + row] = acc[j];
-        __syncthreads();
-        epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt);
-        __syncthreads();
     }
-    if (threadIdx.x == 0) a.counters[nt * MT + mt] = 0;
+    cluster_sync_all();                                  // partials stay alive until read
 }
 
 // ------------------------------------------------------------------ host side
@@ -270,14 +249,16 @@ int gemm_pick_tile_n(int M) {
     return 256;
 }
 
+// Split-K factor: a power of two <= 8 (the splits of a tile form one cluster),
+// only for small token tiles (TN <= 64; larger tiles have enough tiles to fill
+// the GPU), with all CTAs resident in one wave (2 per SM) and >= 2 K blocks each.
 int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms) {
+    if (tile_n > 64) return 1;
     const int ntiles = (N / TM) * ((M + tile_n - 1) / tile_n);
-    const int per_sm = tile_n <= 64 ? 2 : 1;
-    const int slots = num_sms * per_sm;
+    const int slots = num_sms * 2;
     const int KB = K / BK;
-    int s = slots / ntiles;
-    if (s < 1) s = 1;
-    if (s > KB / 2) s = KB / 2 > 0 ? KB / 2 : 1;   // >= 2 K blocks per split
+    int s = 1;
+    while (s < 8 && ntiles * (2 * s) <= slots && 2 * (2 * s) <= KB) s *= 2;
     return s;
 }
 
@@ -296,11 +277,20 @@ static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     cfg.blockDim = dim3(128, 1, 1);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeClusterDimension;       // split-K reduction cluster
+    attr[na].val.clusterDim.x = 1;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = a.splits;
+    ++na;
+    if (g_use_pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = g_use_pdl ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, gemm_kernel<TN, EPI>, tmA, tmB, a);
 }
 
