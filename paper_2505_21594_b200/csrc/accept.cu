@@ -22,6 +22,7 @@ __global__ void __launch_bounds__(ACC_THREADS) row_stats_kernel(const __grid_con
     pdl_launch_dependents();
     pdl_wait();
     const int row = blockIdx.x;
+    ktrace_mark(a.ktrace, a.ktrace_id, 0);
     if (a.req[row / a.G].status_in != 0) return;
     row_stats_body<ACC_THREADS>(a, row, blockIdx.y, threadIdx.x, S, CtaSync{});
 }
@@ -31,6 +32,8 @@ __global__ void __launch_bounds__(ACC_THREADS) accept_kernel(const __grid_consta
     pdl_launch_dependents();
     pdl_wait();
     accept_body<ACC_THREADS>(a, blockIdx.x, blockIdx.y, threadIdx.x, S, CtaSync{});
+    __syncthreads();
+    ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 
 cudaError_t accept_launch(const AcceptArgs& a, cudaStream_t st) {

@@ -16,7 +16,9 @@ __global__ void __launch_bounds__(128) attn_kernel(const __grid_constant__ AttnA
     __shared__ AttnSmem<D> S;
     pdl_launch_dependents();   // the next GEMM may start streaming its weights now
     pdl_wait();
+    ktrace_mark(a.ktrace, a.ktrace_id, 0);
     attn_page_body<D>(a, blockIdx.x, blockIdx.y, threadIdx.x, S, AttnCtaSync{});
+    ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 
 template <int D>

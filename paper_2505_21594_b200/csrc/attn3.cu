@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     const int S = gridDim.x, r = blockIdx.x, bh = blockIdx.y;
     const int b = bh / a.n_heads, h = bh % a.n_heads;
     const int G = a.G;
+    ktrace_mark(a.ktrace, a.ktrace_id, 0);
     pdl_launch_dependents();
     pdl_wait();
     const int ctx = a.ctx[b];
@@ -300,7 +301,10 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
         else
             fO[j * A3_D + d] = O;
     }
-    if (S == 1) return;
+    if (S == 1) {
+        ktrace_mark(a.ktrace, a.ktrace_id, 1);
+        return;
+    }
     cluster_sync3();                                           // split partials visible cluster-wide
     if (cluster_rank3() == 0) {
         for (int i = tid; i < G * A3_D; i += 128) {
@@ -328,6 +332,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
         }
     }
     cluster_sync3();                                           // keep partials alive until merged
+    ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 
 int attn3_splits(int B, int H, int max_pages, int num_sms) {

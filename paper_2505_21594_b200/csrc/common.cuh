@@ -148,6 +148,16 @@ __device__ __forceinline__ float ld_dsmem_f32(const void* local_ptr, uint32_t ra
     return v;
 }
 
+// ------------------------------------------------- per-launch timeline trace
+// [first CTA start, last CTA end] of a launch in globaltimer ns (SV_KTRACE)
+__device__ __forceinline__ void ktrace_mark(unsigned long long* tr, int id, int end) {
+    if (tr && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        atomicMin(&tr[2 * id + end], end ? ~t : t);   // end stored complemented (buffer init ~0)
+    }
+}
+
 // ------------------------------------------------------- programmatic launch
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() {

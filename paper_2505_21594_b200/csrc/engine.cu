@@ -224,6 +224,8 @@ struct sv_engine {
     sv_ticket* inflight = nullptr;
     bool poisoned = false;
     std::vector<ProfRec>* prof = nullptr;
+    unsigned long long* ktrace = nullptr;       // SV_KTRACE: per-launch [start, ~end] globaltimer
+    std::vector<std::pair<int, int>> kmeta;     // (kind, layer) of each traced launch
     std::mutex mu;
 };
 
@@ -404,6 +406,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     CK(cudaStreamCreateWithFlags(&e->s_exit, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
+    if (getenv("SV_KTRACE")) CK(cudaMalloc((void**)&e->ktrace, 1024 * 2 * sizeof(unsigned long long)));
     *out = e;
     return SV_OK;
 }
@@ -558,12 +561,20 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
     do {                                                \
         cudaEvent_t _a = pbeg(s);                       \
         if ((r = (x)) != cudaSuccess) return r;         \
+        if (e->ktrace) {                                \
+            e->kmeta.resize(nl + 1);                    \
+            e->kmeta[nl] = {kind, layer};               \
+        }                                               \
         ++nl;                                           \
         pend(_a, kind, layer, s, bytes, flops);         \
     } while (0)
 
+    if (e->ktrace && (r = cudaMemsetAsync(e->ktrace, 0xFF, 1024 * 2 * sizeof(unsigned long long), st)) != cudaSuccess)
+        return r;
     EmbedArgs ea{(const int32_t*)(e->meta_dev + e->off_tok), e->embed, e->norm_attn[0], e->h, e->u, ssq_at(e, 0, 0), M,
                  e->MP, d};
+    ea.ktrace = e->ktrace;
+    ea.ktrace_id = nl;
     LAUNCH(SV_K_EMBED, -1, st, Md * 2 + d * 2 + Md * 6 + (d / 128) * M * 4.0, 0.0, embed_launch(ea, st));
     double attn_bytes = Md * 6, attn_flops = 0;
     {
@@ -581,6 +592,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
         a.splits = gemm_pick_splits(N, K, M, tn, e->num_sms);
         a.ws = exit_ws ? e->ws_exit : e->ws_main;
         a.counters = exit_ws ? e->cnt_exit : e->cnt_main;
+        a.ktrace = e->ktrace;
+        a.ktrace_id = nl;
         return gemm_launch(epi, tn, A, B, a, s);
     };
     auto lm_and_accept = [&](cudaStream_t s, bool is_exit) -> cudaError_t {
@@ -600,6 +613,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
         aa.B = n; aa.G = G; aa.V = V; aa.nch = e->acc_nch; aa.chunk = e->acc_chunk;
         aa.exit_layer = is_exit ? exit_layer : L;
         aa.is_final = is_exit ? 0 : 1;
+        aa.ktrace = e->ktrace;
+        aa.ktrace_id = nl;
         {
             cudaEvent_t _a = pbeg(s);
             if ((q = accept_launch(aa, s)) != cudaSuccess) return q;
@@ -629,6 +644,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             aa.B = n; aa.G = G; aa.n_heads = e->H; aa.head_dim = e->D; aa.d_model = d; aa.n_layers = L;
             aa.layer = l; aa.page_tokens = e->cfg.page_tokens; aa.nchunk = nchunk;
             aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)e->D));
+            aa.ktrace = e->ktrace;
+            aa.ktrace_id = nl;
             LAUNCH(SV_K_ATTN, l, st, attn_bytes, attn_flops,
                    e->D == 128 ? attn3_launch(aa, attn3_splits(n, e->H, nchunk, e->num_sms), st)
                                : attn_launch(aa, st));
@@ -1075,6 +1092,19 @@ extern "C" sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us) {
     }
     t->final_done = true;
     if (e->opts.fused && e->last_plan && e->last_plan->d_trace) fused_dump_trace(e->last_plan, getenv("SV_TRACE"));
+    if (e->ktrace && getenv("SV_KTRACE")) {   // per-launch timeline of this step
+        std::vector<unsigned long long> tr(2 * e->kmeta.size());
+        if (cudaMemcpy(tr.data(), e->ktrace, tr.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            FILE* fp = fopen(getenv("SV_KTRACE"), "w");
+            if (fp) {
+                fprintf(fp, "id,kind,layer,start_ns,end_ns\n");
+                for (size_t i = 0; i < e->kmeta.size(); ++i)
+                    fprintf(fp, "%zu,%d,%d,%llu,%llu\n", i, e->kmeta[i].first, e->kmeta[i].second, tr[2 * i],
+                            ~tr[2 * i + 1]);
+                fclose(fp);
+            }
+        }
+    }
     e->inflight = nullptr;
     return SV_OK;
 }

@@ -62,7 +62,7 @@ struct GemmCfg {
     static constexpr int SMEM = 1024 + STAGES * STAGE + AUX;
     static_assert(STAGES >= 2, "pipeline too shallow");
     static_assert(EPI_CHUNK * TM * 4 <= STAGES * STAGE, "epilogue tile must fit the ring");
-    static_assert(TN > 64 || (TN + EPI_CHUNK) * TM * 4 <= STAGES * STAGE, "split partial + epilogue tile");
+    static_assert((TN + EPI_CHUNK) * TM * 4 <= STAGES * STAGE, "split partial + epilogue tile");
 };
 
 struct GemmCtaSync {
@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(128, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nt = blockIdx.x, mt = blockIdx.y, split = blockIdx.z;
+    ktrace_mark(a.ktrace, a.ktrace_id, 0);
     const int NT = gridDim.x, MT = gridDim.y;
     const int n0 = nt * TM, m0 = mt * TN;
     const int KB = a.K / BK;
@@ -188,7 +189,10 @@ __global__ void __launch_bounds__(128, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
-    if (direct) return;
+    if (direct) {
+        ktrace_mark(a.ktrace, a.ktrace_id, 1);
+        return;
+    }
 
     // ---------------- split-K through distributed shared memory: the splits of a
     // tile are one thread-block cluster (dims 1 x 1 x S, rank = split); rank 0 adds
@@ -217,6 +221,7 @@ __global__ void __launch_bounds__(128, 1)
         }
     }
     cluster_sync_all();                                  // partials stay alive until read
+    ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 
 // ------------------------------------------------------------------ host side
@@ -253,9 +258,8 @@ int gemm_pick_tile_n(int M) {
 // only for small token tiles (TN <= 64; larger tiles have enough tiles to fill
 // the GPU), with all CTAs resident in one wave (2 per SM) and >= 2 K blocks each.
 int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms) {
-    if (tile_n > 64) return 1;
     const int ntiles = (N / TM) * ((M + tile_n - 1) / tile_n);
-    const int slots = num_sms * 2;
+    const int slots = num_sms * (tile_n <= 64 ? 2 : 1);
     const int KB = K / BK;
     int s = 1;
     while (s < 8 && ntiles * (2 * s) <= slots && 2 * (2 * s) <= KB) s *= 2;

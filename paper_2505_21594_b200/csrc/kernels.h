@@ -55,6 +55,8 @@ struct GemmArgs {
     int d_ff;
     // EPI_LOGITS
     float* logits;        // [M][N]
+    unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
+    int ktrace_id = 0;
 };
 
 // Encodes a 2D bf16 K-major tensor map (rows x K), box = 64 x box_rows, SW128.
@@ -78,6 +80,8 @@ struct AttnArgs {
     int pt_stride;
     int B, G, n_heads, head_dim, d_model, n_layers, layer, page_tokens, nchunk;
     float scale_log2;     // log2(e) / sqrt(head_dim)
+    unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
+    int ktrace_id = 0;
 };
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st);
 // v3 (head_dim 128): mma.sync bf16 tensor-core tiles, per-warp cp.async rings,
@@ -113,6 +117,8 @@ struct AcceptArgs {
     sv_exit_result* out;    // [B] device
     int B, G, V, nch, chunk;
     int exit_layer, is_final;
+    unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
+    int ktrace_id = 0;
 };
 cudaError_t accept_launch(const AcceptArgs& a, cudaStream_t st);
 int accept_chunks(int V, int* chunk);
@@ -126,6 +132,8 @@ struct EmbedArgs {
     void* u;             // bf16 [MP][d]
     float* ssq;          // [d/128][MP]
     int M, MP, d;
+    unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
+    int ktrace_id = 0;
 };
 cudaError_t embed_launch(const EmbedArgs& a, cudaStream_t st);
 

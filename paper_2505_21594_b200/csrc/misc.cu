@@ -11,6 +11,7 @@ bool g_use_pdl = true;
 // ssq[t][m] = sum of h^2 over the 128-column tile t (RMSNorm statistics for layer 1).
 __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ EmbedArgs a) {
     __shared__ float sRed[4];
+    ktrace_mark(a.ktrace, a.ktrace_id, 0);
     pdl_launch_dependents();
     pdl_wait();
     const int m = blockIdx.x, t = blockIdx.y;
@@ -24,6 +25,7 @@ __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ Embe
     if ((threadIdx.x & 31) == 0) sRed[threadIdx.x >> 5] = s;
     __syncthreads();
     if (threadIdx.x == 0) a.ssq[(size_t)t * a.MP + m] = (sRed[0] + sRed[1]) + (sRed[2] + sRed[3]);
+    ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 
 cudaError_t embed_launch(const EmbedArgs& a, cudaStream_t st) {
