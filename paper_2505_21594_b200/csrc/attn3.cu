@@ -27,7 +27,7 @@
 namespace sv {
 
 constexpr int A3_D = 128;            // head dim (the tensor-core path is specialised for Dh = 128)
-constexpr int A3_CHUNK = 16;         // keys per chunk (small smem: the next GEMM's CTAs co-reside)
+constexpr int A3_CHUNK = 32;         // keys per chunk
 constexpr int A3_WARPS = 4;
 constexpr int A3_ROWB = A3_D * 2;    // 256 B per K / V row
 constexpr int A3_CHB = A3_CHUNK * A3_ROWB;              // 8 KB per K (or V) chunk
@@ -127,18 +127,18 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     __syncthreads();
 
     // this warp's chunks: c = warp, warp + 4, ... over the CTA's 2*np chunks
-    const int nchunks = (64 / A3_CHUNK) * np;
+    const int nchunks = 2 * np;
     const size_t plane = (size_t)a.n_heads * a.page_tokens * A3_D;
     const uint32_t wring = s_ring + warp * 2 * A3_STAGE;
     auto issue = [&](int ci, int stage) {
-        const int pg = ci / (64 / A3_CHUNK), koff = (ci % (64 / A3_CHUNK)) * A3_CHUNK;
+        const int pg = ci >> 1, koff = (ci & 1) * A3_CHUNK;
         const bf16* kb = reinterpret_cast<const bf16*>(a.kv_pool) +
                          (((size_t)sBlk[pg] * a.n_layers + a.layer) * 2) * plane + (size_t)h * a.page_tokens * A3_D +
                          (size_t)koff * A3_D;
         const bf16* vb = kb + plane;
         const uint32_t dk = wring + stage * A3_STAGE, dv = dk + A3_CHB;
 #pragma unroll
-        for (int u = 0; u < (A3_CHUNK * 16) / 32; ++u) {      // CHUNK*16 16-byte pieces per matrix
+        for (int u = 0; u < (A3_CHUNK * 16) / 32; ++u) {      // 512 16-byte pieces per matrix
             const int piece = lane + 32 * u, row = piece >> 4, c = piece & 15;
             cp_async16(dk + swz(row, c), kb + row * A3_D + c * 8);
             cp_async16(dv + swz(row, c), vb + row * A3_D + c * 8);
@@ -183,15 +183,14 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
             }
             __syncwarp();
         }
-        // ---- S = Q K^T  (16 x CHUNK)
-        constexpr int NTS = A3_CHUNK / 8;                     // n-tiles of S
-        float sacc[NTS][4];
+        // ---- S = Q K^T  (16 x 32)
+        float sacc[4][4];
 #pragma unroll
-        for (int n = 0; n < NTS; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
+        for (int n = 0; n < 4; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
 #pragma unroll
-            for (int np2 = 0; np2 < NTS / 2; ++np2) {        // n-tiles 2*np2, 2*np2+1
+            for (int np2 = 0; np2 < 2; ++np2) {              // n-tiles 2*np2, 2*np2+1
                 uint32_t b0, b1, b2, b3;
                 const int key = 16 * np2 + 8 * (lane >> 4) + (lane & 7), c = 2 * ks + ((lane >> 3) & 1);
                 ldsm_x4(sk + swz(key, c), b0, b1, b2, b3);
@@ -202,7 +201,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
         // ---- causal mask + online softmax (rows g and g+8 of this thread)
         float mnew[2] = {mrow[0], mrow[1]};
 #pragma unroll
-        for (int n = 0; n < NTS; ++n)
+        for (int n = 0; n < 4; ++n)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int j = (e < 2) ? row0 : row1;
@@ -218,9 +217,9 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
         float alpha[2], psum[2] = {0.f, 0.f};
 #pragma unroll
         for (int x = 0; x < 2; ++x) alpha[x] = (mrow[x] == -INFINITY) ? 0.f : exp2f(mrow[x] - mnew[x]);
-        uint32_t pa[NTS / 2][4];                              // P as A fragments (k-steps of 16 keys)
+        uint32_t pa[2][4];                                    // P as A fragments (2 k-steps of 16 keys)
 #pragma unroll
-        for (int n = 0; n < NTS; ++n) {
+        for (int n = 0; n < 4; ++n) {
             float p[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -248,7 +247,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
         }
         // ---- O += P V  (16 x 128), V via ldmatrix.trans
 #pragma unroll
-        for (int kk = 0; kk < NTS / 2; ++kk) {
+        for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
             for (int nd = 0; nd < 16; nd += 2) {
                 uint32_t b0, b1, b2, b3;
