@@ -4,11 +4,14 @@
 // on dedicated warps while the tensor core already accumulates tile i+1 into the
 // second TMEM buffer.
 //
-//   warps 0-3  epilogue (TMEM lane quarter = warp): TMEM -> smem -> fused op
-//              (gemm_epi.cuh), released per tile through tmem_empty[buf]
-//   warp 4     TMA producer: continuous STAGES-deep ring over all (tile, k-block)
+//   warps 0-7  epilogue in two groups of four (group g = warps 4g..4g+3, TMEM lane
+//              quarter = warp % 4) taking alternate 16-token chunks of the tile:
+//              TMEM -> smem -> fused op (gemm_epi.cuh); per-tile metadata (rstd,
+//              positions, KV pages) is staged in smem before the accumulator is
+//              ready; the tile is released through tmem_empty[buf]
+//   warp 8     TMA producer: continuous STAGES-deep ring over all (tile, k-block)
 //              of this CTA (weights evict-first, activations evict-last)
-//   warp 5     tcgen05.mma issuer (M = 128 weight rows, N = TILE_N tokens)
+//   warp 9     tcgen05.mma issuer (M = 128 weight rows, N = TILE_N tokens)
 // Tiles are ordered n-major, m-minor (tile = n*MT + m) and dealt round-robin, so
 // the m-tiles that share one weight tile run on neighbouring CTAs at the same time
 // and the weight tile is read from HBM once (L2 serves the others).
@@ -26,7 +29,8 @@ template <int TN>
 struct GBCfg {
     static constexpr int B_STAGE = TN * GB_BK * 2;
     static constexpr int STAGE = GB_A + B_STAGE;
-    static constexpr int EPI = EPI_CHUNK * GB_TM * 4 + TN * 4 + 4 * EPI_CHUNK * 4;
+    // two groups x (sOut [16][128] f32 + sRed [4][16]) + sR, sPos, sBlk [TN]
+    static constexpr int EPI = 2 * (EPI_CHUNK * GB_TM * 4 + 4 * EPI_CHUNK * 4) + 3 * TN * 4;
     static constexpr int AUX = 512;
     static constexpr int RAW = (227 * 1024 - 1024 - EPI - AUX) / STAGE;
     static constexpr int STAGES = RAW > 8 ? 8 : RAW;
@@ -35,12 +39,16 @@ struct GBCfg {
     static_assert(STAGES >= 3 && TCOLS <= 512, "config");
 };
 
-struct EpiBar {
-    __device__ void operator()() const { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+constexpr int GB_EPI_WARPS = 8, GB_THREADS = (GB_EPI_WARPS + 2) * 32;
+
+struct EpiBar {   // one epilogue group (named barrier 1 + group)
+    int id;
+    __device__ void operator()() const { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 };
+__device__ __forceinline__ void epi_all_bar() { asm volatile("bar.sync 3, 256;" ::: "memory"); }
 
 template <int TN, int EPI>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(GB_THREADS, 1)
     gemm_big_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ GemmArgs a) {
     using C = GBCfg<TN>;
@@ -48,9 +56,11 @@ __global__ void __launch_bounds__(192, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + C::STAGES * GB_A;
-    float* sOut = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE);   // [EPI_CHUNK][128]
-    float* sR = sOut + EPI_CHUNK * GB_TM;                                   // [TN]
-    float* sRed = sR + TN;                                                  // [4][EPI_CHUNK]
+    float* sOut0 = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE);  // 2 x [EPI_CHUNK][128]
+    float* sRed0 = sOut0 + 2 * EPI_CHUNK * GB_TM;                          // 2 x [4][EPI_CHUNK]
+    float* sR = sRed0 + 2 * 4 * EPI_CHUNK;                                 // [TN]
+    int* sPos = reinterpret_cast<int*>(sR + TN);                           // [TN]
+    int* sBlk = sPos + TN;                                                 // [TN]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE + C::EPI);
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
@@ -61,7 +71,7 @@ __global__ void __launch_bounds__(192, 1)
     const int NT = a.N / GB_TM, MT = (a.M + TN - 1) / TN, T = NT * MT;
     const int KB = a.K / GB_BK;
     ktrace_mark(a.ktrace, a.ktrace_id, 0);
-    if (warp == 4 && lane == 0) {
+    if (warp == 8 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         for (int s = 0; s < C::STAGES; ++s) {
@@ -74,14 +84,14 @@ __global__ void __launch_bounds__(192, 1)
         }
         fence_mbar_init();
     }
-    if (warp == 5) tmem_alloc(tmem_slot, C::TCOLS);
+    if (warp == 9) tmem_alloc(tmem_slot, C::TCOLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     pdl_launch_dependents();
 
-    if (warp == 4) {
+    if (warp == 8) {
         if (lane == 0) {   // ------------------------------------------ producer
             const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
             int it = 0;
@@ -101,7 +111,7 @@ __global__ void __launch_bounds__(192, 1)
                 }
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         if (lane == 0) {   // ------------------------------------------ MMA issuer
             constexpr uint32_t idesc = umma_idesc_bf16(GB_TM, TN);
             int it = 0, seg = 0;
@@ -124,20 +134,25 @@ __global__ void __launch_bounds__(192, 1)
                 umma_commit(&tfull[buf]);
             }
         }
-    } else {               // ------------------------------------------ epilogue warps 0-3
-        EpiBar bar;
-        const int r = threadIdx.x;                         // 0..127 = tile row (TMEM lane)
+    } else {               // ------------------------------------------ epilogue warps 0-7
+        const int grp = warp >> 2, tid = threadIdx.x;     // tid 0..255
+        const EpiBar bar{1 + grp};
+        const int r = tid & 127;                           // tile row (TMEM lane)
+        float* sOut = sOut0 + grp * EPI_CHUNK * GB_TM;
+        float* sRed = sRed0 + grp * 4 * EPI_CHUNK;
         pdl_wait();                                        // epilogue inputs come from earlier kernels
         int seg = 0;
         for (int t = blockIdx.x; t < T; t += gridDim.x, ++seg) {
             const int buf = seg & 1;
             const int nt = t / MT, n0 = nt * GB_TM, m0 = (t % MT) * TN;
-            epi_rstd(a, sR, m0, TN, r, 128);
+            epi_rstd(a, sR, m0, TN, tid, 256);             // overlaps the tile's MMA
+            if constexpr (EPI == EPI_QKV) epi_meta(a, sPos, sBlk, m0, TN, tid, 256);
+            epi_all_bar();
             mbar_wait(&tfull[buf], (seg >> 1) & 1);
             tc_fence_after();
-            const uint32_t tb = tmem + (static_cast<uint32_t>(warp * 32) << 16) + buf * TN;
-            for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
-                if (m0 + c0 >= a.M) break;                 // uniform over the 128 threads
+            const uint32_t tb = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + buf * TN;
+            for (int c0 = grp * EPI_CHUNK; c0 < TN; c0 += 2 * EPI_CHUNK) {
+                if (m0 + c0 >= a.M) break;                 // uniform over the group
                 uint32_t v[16];
                 tmem_ld_32x32b_x16(tb + c0, v);
                 tmem_ld_wait();
@@ -145,16 +160,16 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) sOut[j * GB_TM + r] = __uint_as_float(v[j]);
                 bar();
-                epi_apply<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt, r, bar);
+                epi_apply<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt, r, bar, sPos, sBlk);
             }
             tc_fence_before();
-            bar();
-            if (r == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
+            epi_all_bar();                                 // also guards sR / sPos reuse
+            if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) tmem_dealloc(tmem, C::TCOLS);
+    if (warp == 9) tmem_dealloc(tmem, C::TCOLS);
     ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 
@@ -175,7 +190,7 @@ static cudaError_t big_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const G
     const int T = (a.N / GB_TM) * ((a.M + TN - 1) / TN);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(T < sms ? T : sms, 1, 1);
-    cfg.blockDim = dim3(192, 1, 1);
+    cfg.blockDim = dim3(GB_THREADS, 1, 1);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr1[1];

@@ -18,9 +18,12 @@ namespace sv {
 constexpr int EPI_TM = 128;       // weight rows per tile
 constexpr int EPI_CHUNK = 16;     // token columns per epilogue pass
 
+// sPos / sBlk (optional, EPI_QKV): position and KV page of token m0 + t, staged in
+// shared memory once per tile (epi_meta) instead of re-gathered per chunk.
 template <int EPI, class Sync>
 __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, const float* sR, float* sRed,
-                                          int tok0, int m0, int n0, int nt, int r, Sync sync) {
+                                          int tok0, int m0, int n0, int nt, int r, Sync sync,
+                                          const int* sPos = nullptr, const int* sBlk = nullptr) {
     constexpr int TM = EPI_TM;
     const int warp = r >> 5, lane = r & 31;
     if constexpr (EPI == EPI_QKV) {
@@ -35,9 +38,17 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
         // compiler cannot move loads across the stores of the previous token)
         int pos[EPI_CHUNK], blk[EPI_CHUNK];
         float2 cs[EPI_CHUNK];
+        if (sPos) {
 #pragma unroll
-        for (int j = 0; j < EPI_CHUNK; ++j) pos[j] = (j < nv) ? a.meta.pos[tok0 + j] : 0;
-        if (sec >= 1) {
+            for (int j = 0; j < EPI_CHUNK; ++j) {
+                pos[j] = (j < nv) ? sPos[tok0 - m0 + j] : 0;
+                blk[j] = (j < nv) ? sBlk[tok0 - m0 + j] : 0;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < EPI_CHUNK; ++j) pos[j] = (j < nv) ? a.meta.pos[tok0 + j] : 0;
+        }
+        if (sec >= 1 && !sPos) {
             int req[EPI_CHUNK];
 #pragma unroll
             for (int j = 0; j < EPI_CHUNK; ++j) req[j] = (j < nv) ? a.meta.row_req[tok0 + j] : 0;
@@ -138,6 +149,21 @@ __device__ __forceinline__ void epi_rstd(const GemmArgs& a, float* sR, int m0, i
             rs = 1.0f / sqrtf(s * a.inv_d + a.eps);
         }
         sR[t] = rs;
+    }
+}
+
+// position and KV page of tokens m0 .. m0+tn-1 (EPI_QKV metadata, see epi_apply)
+__device__ __forceinline__ void epi_meta(const GemmArgs& a, int* sPos, int* sBlk, int m0, int tn, int r,
+                                         int nthreads) {
+    for (int t = r; t < tn; t += nthreads) {
+        const int tok = m0 + t;
+        int p = 0, b = 0;
+        if (tok < a.M) {
+            p = a.meta.pos[tok];
+            b = a.meta.page_table[a.meta.row_req[tok] * a.meta.pt_stride + p / a.page_tokens];
+        }
+        sPos[t] = p;
+        sBlk[t] = b;
     }
 }
 
