@@ -10,7 +10,8 @@
 //
 // * grid (splits, B*H); a CTA owns a contiguous run of 64-key pages; each of its
 //   4 warps streams every 4th 32-key chunk with its own 2-stage cp.async ring
-//   (16-byte copies into an XOR-swizzled layout, conflict-free ldmatrix);
+//   (16-byte copies into an XOR-swizzled layout, conflict-free ldmatrix); the
+//   first two chunks of cached rows are requested before griddepcontrol.wait;
 // * per chunk (FlashAttention-2 register pipeline): S = Q K^T (4 n-tiles x 8
 //   k-steps), causal mask, online softmax in the log2 domain on the accumulator
 //   fragments, P (bf16, straight from the S fragments) times V via ldmatrix.trans;
@@ -99,13 +100,48 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     const int G = a.G;
     ktrace_mark(a.ktrace, a.ktrace_id, 0);
     pdl_launch_dependents();
-    pdl_wait();
+    // lengths and page tables are host-written before the step; the cache rows
+    // below ctx were written by earlier steps -> their loads are issued before
+    // griddepcontrol.wait and overlap the QKV GEMM; q and the gamma+1 new rows
+    // (this step's QKV epilogue) are only touched after it.
     const int ctx = a.ctx[b];
     const int T = ctx + G;
     const int npg = (T + 63) / 64;
     const int p0 = (int)((long long)npg * r / S), p1 = (int)((long long)npg * (r + 1) / S);
     const int np = p1 - p0;
     for (int i = tid; i < np; i += 128) sBlk[i] = a.page_table[b * a.pt_stride + p0 + i];
+    __syncthreads();
+
+    // this warp's chunks: ci = warp + 4 * it over the CTA's 2*np chunks, 2-deep ring
+    const int nchunks = 2 * np;
+    const int n_my = nchunks > warp ? (nchunks - warp + A3_WARPS - 1) / A3_WARPS : 0;
+    const size_t plane = (size_t)a.n_heads * a.page_tokens * A3_D;
+    const uint32_t wring = s_ring + warp * 2 * A3_STAGE;
+    auto issue = [&](int ci, int stage) {
+        const int pg = ci >> 1, koff = (ci & 1) * A3_CHUNK;
+        const bf16* kb = reinterpret_cast<const bf16*>(a.kv_pool) +
+                         (((size_t)sBlk[pg] * a.n_layers + a.layer) * 2) * plane + (size_t)h * a.page_tokens * A3_D +
+                         (size_t)koff * A3_D;
+        const bf16* vb = kb + plane;
+        const uint32_t dk = wring + stage * A3_STAGE, dv = dk + A3_CHB;
+#pragma unroll
+        for (int u = 0; u < (A3_CHUNK * 16) / 32; ++u) {      // 512 16-byte pieces per matrix
+            const int piece = lane + 32 * u, row = piece >> 4, c = piece & 15;
+            cp_async16(dk + swz(row, c), kb + row * A3_D + c * 8);
+            cp_async16(dv + swz(row, c), vb + row * A3_D + c * 8);
+        }
+        cp_commit();
+    };
+    // chunk ci holds only cached rows iff its last key < ctx; such chunks form a
+    // prefix of this warp's sequence, so commit order stays the chunk order
+    int pre = 0;
+    while (pre < 2 && pre < n_my && (p0 * 64 + (warp + A3_WARPS * pre + 1) * A3_CHUNK) <= ctx) {
+        issue(warp + A3_WARPS * pre, pre);
+        ++pre;
+    }
+    pdl_wait();
+    for (int it = pre; it < 2 && it < n_my; ++it) issue(warp + A3_WARPS * it, it);
+
     // Q (pre-scaled by log2(e)/sqrt(Dh)) -> bf16, rows >= G zero, swizzled
     for (int i = tid; i < 16 * (A3_D / 8); i += 128) {
         const int row = i / (A3_D / 8), c = i % (A3_D / 8);
@@ -126,26 +162,6 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     }
     __syncthreads();
 
-    // this warp's chunks: c = warp, warp + 4, ... over the CTA's 2*np chunks
-    const int nchunks = 2 * np;
-    const size_t plane = (size_t)a.n_heads * a.page_tokens * A3_D;
-    const uint32_t wring = s_ring + warp * 2 * A3_STAGE;
-    auto issue = [&](int ci, int stage) {
-        const int pg = ci >> 1, koff = (ci & 1) * A3_CHUNK;
-        const bf16* kb = reinterpret_cast<const bf16*>(a.kv_pool) +
-                         (((size_t)sBlk[pg] * a.n_layers + a.layer) * 2) * plane + (size_t)h * a.page_tokens * A3_D +
-                         (size_t)koff * A3_D;
-        const bf16* vb = kb + plane;
-        const uint32_t dk = wring + stage * A3_STAGE, dv = dk + A3_CHB;
-#pragma unroll
-        for (int u = 0; u < (A3_CHUNK * 16) / 32; ++u) {      // 512 16-byte pieces per matrix
-            const int piece = lane + 32 * u, row = piece >> 4, c = piece & 15;
-            cp_async16(dk + swz(row, c), kb + row * A3_D + c * 8);
-            cp_async16(dv + swz(row, c), vb + row * A3_D + c * 8);
-        }
-        cp_commit();
-    };
-
     // Q A-fragments for the 8 k-steps
     uint32_t qa[8][4];
 #pragma unroll
@@ -160,16 +176,12 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
     const int row0 = g, row1 = g + 8;
 
-    int it = 0;
-    if (warp < nchunks) issue(warp, 0);
-    for (int ci = warp; ci < nchunks; ci += A3_WARPS, ++it) {
-        const int stage = it & 1;
-        if (ci + A3_WARPS < nchunks) {
-            issue(ci + A3_WARPS, stage ^ 1);
+    for (int it = 0; it < n_my; ++it) {
+        const int ci = warp + A3_WARPS * it, stage = it & 1;
+        if (it + 1 < n_my)
             cp_wait<1>();
-        } else {
+        else
             cp_wait<0>();
-        }
         __syncwarp();
         const uint32_t sk = wring + stage * A3_STAGE, sv = sk + A3_CHB;
         const int kabs0 = (p0 * 64) + ci * A3_CHUNK;
@@ -258,6 +270,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
             }
         }
         __syncwarp();
+        if (it + 2 < n_my) issue(ci + 2 * A3_WARPS, stage);   // refill the stage just consumed
     }
 
     // ---- merge the 4 warps (warp order) through shared memory (aliases the rings)

@@ -178,6 +178,7 @@ struct sv_engine {
     sv_model_cfg cfg;
     sv_engine_opts opts;
     int device, num_sms;
+    int pf_depth = 4;                           // GemmArgs::pf_depth (env SV_PF)
     // weights
     void *embed, *lm_head, *norm_final;
     std::vector<void*> w_qkv, w_o, w_gu, w_down, norm_attn, norm_mlp;
@@ -383,6 +384,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     e->opts = *opts;
     e->device = device;
     CK(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device));
+    if (const char* pf = getenv("SV_PF")) e->pf_depth = atoi(pf);
     e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
     e->L = cfg->n_layers; e->d = cfg->d_model; e->F = cfg->d_ff; e->V = cfg->vocab;
     e->H = cfg->n_heads; e->D = cfg->head_dim;
@@ -585,11 +587,19 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
         }
     }
 
+    // nx / nN / nK: the next GEMM on the same stream (its weights are prefetched to L2)
     auto gemm = [&](int epi, const CUtensorMap& A, const CUtensorMap& B, int N, int K, GemmArgs a, cudaStream_t s,
-                    bool exit_ws) -> cudaError_t {
+                    bool exit_ws, int nx = -1, int nN = 0, int nK = 0) -> cudaError_t {
         a.N = N;
         a.K = K;
         a.splits = gemm_pick_splits(N, K, M, tn, e->num_sms);
+        if (nx >= 0 && tn <= 64 && e->pf_depth > 0) {
+            a.pf_map = e->d_tmaps + nx;
+            a.pf_tiles = nN / 128;
+            a.pf_splits = gemm_pick_splits(nN, nK, M, tn, e->num_sms);
+            a.pf_kb = nK / 64;
+            a.pf_depth = e->pf_depth;
+        }
         a.ws = exit_ws ? e->ws_exit : e->ws_main;
         a.counters = exit_ws ? e->cnt_exit : e->cnt_main;
         a.ktrace = e->ktrace;
@@ -632,7 +642,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             a.ssq_in = ssq_at(e, l, 0);
             a.qbuf = e->qbuf;
             LAUNCH(SV_K_QKV, l, st, gemm_bytes(3.0 * d, d, Md * 8 + (d / 128) * M * 4.0), 2.0 * M * 3.0 * d * d,
-                   gemm(EPI_QKV, e->tm_qkv[l], tma[0], 3 * d, d, a, st, false));
+                   gemm(EPI_QKV, e->tm_qkv[l], tma[0], 3 * d, d, a, st, false, L + l, d, d));
         }
         {   // attention
             AttnArgs aa = {};
@@ -654,14 +664,14 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             GemmArgs a = base_args(e, M);
             a.h = e->h; a.g_out = e->norm_mlp[l]; a.u_out = e->u; a.ssq_out = ssq_at(e, l, 1);
             LAUNCH(SV_K_O, l, st, gemm_bytes(d, d, Md * 10 + (d / 128) * M * 4.0), 2.0 * M * d * d,
-                   gemm(EPI_RESID, e->tm_o[l], tma[1], d, d, a, st, false));
+                   gemm(EPI_RESID, e->tm_o[l], tma[1], d, d, a, st, false, 2 * L + l, 2 * F, d));
         }
         {   // gate/up + SwiGLU
             GemmArgs a = base_args(e, M);
             a.ssq_in = ssq_at(e, l, 1);
             a.act = e->act;
             LAUNCH(SV_K_GU, l, st, gemm_bytes(2.0 * F, d, (double)M * F * 2 + (d / 128) * M * 4.0),
-                   2.0 * M * 2.0 * F * d, gemm(EPI_SWIGLU, e->tm_gu[l], tma[0], 2 * F, d, a, st, false));
+                   2.0 * M * 2.0 * F * d, gemm(EPI_SWIGLU, e->tm_gu[l], tma[0], 2 * F, d, a, st, false, 3 * L + l, d, F));
         }
         {   // down + residual (+ early-exit copy with the final gain)
             GemmArgs a = base_args(e, M);
@@ -674,7 +684,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             }
             a.ssq_out = ssq_at(e, l + 1, 0);
             LAUNCH(SV_K_DOWN, l, st, gemm_bytes(d, F, Md * (l + 1 == exit_layer ? 12 : 10) + (d / 128) * M * 4.0),
-                   2.0 * M * d * F, gemm(EPI_RESID, e->tm_down[l], tma[2], d, F, a, st, false));
+                   2.0 * M * d * F,
+                   gemm(EPI_RESID, e->tm_down[l], tma[2], d, F, a, st, false, l + 1 < L ? l + 1 : 4 * L, l + 1 < L ? 3 * d : V, d));
         }
         if (l + 1 == exit_layer) {   // fork the early exit (S10-S11)
             if ((r = cudaEventRecord(e->ev_fork, st)) != cudaSuccess) return r;
@@ -1246,12 +1257,15 @@ extern "C" sv_status sv_debug_profile_step(sv_engine* e, const sv_verify_req* re
     e->prof = &recs;
     const bool pdl = g_use_pdl;
     g_use_pdl = false;   // serialise kernels so events bracket exactly one launch
+    unsigned long long* kt = e->ktrace;
+    e->ktrace = nullptr;  // the SV_KTRACE timeline records graph replays only
     sv_ticket* t = nullptr;
     sv_status s = sv_verify_submit(e, reqs, n, exit_layer, early, final_, nullptr, &t);
     e->prof = nullptr;
     g_use_pdl = pdl;
+    if (!s) s = sv_ticket_release(t);
+    e->ktrace = kt;
     if (s) return s;
-    if ((s = sv_ticket_release(t))) return s;
     CK(cudaDeviceSynchronize());
     int k = 0;
     for (auto& r : recs) {

@@ -142,6 +142,16 @@ __global__ void __launch_bounds__(128, 1)
             tma_load_2d(&tmA, sA + s * A_STAGE, &full[s], (kb0 + i) * BK, n0, pol_w);
             tma_load_2d(&tmB, sB + s * C::B_STAGE, &full[s], (kb0 + i) * BK, m0, pol_x);
         }
+        if (a.pf_map) {   // next GEMM's first K blocks -> L2 (GemmArgs::pf_map)
+            const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+            const int ncta = gridDim.x * gridDim.y * gridDim.z;
+            for (int c = cta; c < a.pf_tiles * a.pf_splits; c += ncta) {
+                const int tile = c % a.pf_tiles, sp = c / a.pf_tiles;
+                const int k0 = (int)((long long)a.pf_kb * sp / a.pf_splits);
+                const int k1 = min((int)((long long)a.pf_kb * (sp + 1) / a.pf_splits), k0 + a.pf_depth);
+                for (int k = k0; k < k1; ++k) tma_prefetch_l2_2d(a.pf_map, k * BK, tile * TM);
+            }
+        }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer (single thread)
         constexpr uint32_t idesc = umma_idesc_bf16(TM, TN);

@@ -55,6 +55,12 @@ struct GemmArgs {
     int d_ff;
     // EPI_LOGITS
     float* logits;        // [M][N]
+    // L2 prefetch of the next GEMM's weights: the first pf_depth K blocks of every
+    // CTA of the next launch (pf_tiles x pf_splits CTAs, pf_kb K blocks split evenly),
+    // issued once this CTA's own loads are in flight, so HBM keeps streaming through
+    // this grid's tail, the launch gap and the next grid's ramp-up.
+    const CUtensorMap* pf_map = nullptr;    // device copy of the next weight map, or nullptr
+    int pf_tiles = 0, pf_splits = 1, pf_kb = 0, pf_depth = 0;
     unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
     int ktrace_id = 0;
 };
