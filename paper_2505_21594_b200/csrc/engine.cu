@@ -178,7 +178,7 @@ struct sv_engine {
     sv_model_cfg cfg;
     sv_engine_opts opts;
     int device, num_sms;
-    int pf_depth = 4;                           // GemmArgs::pf_depth (env SV_PF)
+    int pf_depth = 0;                           // GemmArgs::pf_depth (env SV_PF)
     // weights
     void *embed, *lm_head, *norm_final;
     std::vector<void*> w_qkv, w_o, w_gu, w_down, norm_attn, norm_mlp;
