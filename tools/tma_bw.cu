@@ -110,8 +110,8 @@ static float run(const CUtensorMap& tm, const uint8_t* base, int mode, int ntile
     return (float)ntiles * 16384.0f * reps / (ms / 1e3f) / 1e9f;
 }
 
-int main() {
-    const int N = 22016, K = 4096;                 // the gate/up matrix of Llama2-7B (180 MB)
+int main(int argc, char** argv) {
+    const int N = argc > 1 ? atoi(argv[1]) : 22016, K = argc > 2 ? atoi(argv[2]) : 4096;   // default: gate/up of Llama2-7B (180 MB)
     const size_t bytes = (size_t)N * K * 2;
     uint8_t* buf;
     cudaMalloc(&buf, bytes);
@@ -127,8 +127,8 @@ int main() {
     enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     uint8_t* act;
-    cudaMalloc(&act, 16 * K * 2);
-    cudaMemset(act, 0, 16 * K * 2);
+    cudaMalloc(&act, 16 * (size_t)K * 2);
+    cudaMemset(act, 0, 16 * (size_t)K * 2);
     cuuint64_t gdb[2] = {(cuuint64_t)K, 16};
     cuuint32_t boxb[2] = {64, 16};
     enc(&g_tmb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, act, gdb, gstr, boxb, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
