@@ -33,7 +33,11 @@ constexpr int A3_WARPS = 4;
 constexpr int A3_ROWB = A3_D * 2;    // 256 B per K / V row
 constexpr int A3_CHB = A3_CHUNK * A3_ROWB;              // 8 KB per K (or V) chunk
 constexpr int A3_STAGE = 2 * A3_CHB;                    // K + V
-constexpr int A3_SMEM = 1024 + A3_WARPS * 2 * A3_STAGE /*rings*/ + 16 * A3_ROWB /*Q bf16*/ + 256;
+template <int NST>   // ring stages per warp: 2 (deep contexts) or 1 (<= 1 chunk per warp: 69 KB, so the
+                     // CTA co-resides with a neighbouring GEMM grid under programmatic dependent launch)
+struct A3Cfg {
+    static constexpr int SMEM = 1024 + A3_WARPS * NST * A3_STAGE /*rings*/ + 16 * A3_ROWB /*Q bf16*/ + 256;
+};
 
 __device__ __forceinline__ uint32_t swz(int row, int chunk16) {          // byte offset in a 256 B-row tile
     return (uint32_t)(row * A3_ROWB + ((chunk16 ^ (row & 7)) << 4));
@@ -79,11 +83,18 @@ __device__ __forceinline__ float ld_dsmem3(const void* p, uint32_t rank) {
     return v;
 }
 
+#define A3_STAMP(k)                                                                                   \
+    if (a.atrace && threadIdx.x == 0 && blockIdx.x == 0 && (blockIdx.y == 0 || blockIdx.y == gridDim.y - 1)) { \
+        unsigned long long _t;                                                                        \
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(_t));                                         \
+        a.atrace[(blockIdx.y == 0 ? 0 : 8) + (k)] = _t;                                               \
+    }
+template <int NST>
 __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t s_ring = smem_u32(smem);                                   // [warp][stage][K|V] 8 KB tiles
-    const uint32_t s_q = s_ring + A3_WARPS * 2 * A3_STAGE;                     // Q bf16 [16][128] swizzled
+    const uint32_t s_q = s_ring + A3_WARPS * NST * A3_STAGE;                     // Q bf16 [16][128] swizzled
     // merge scratch aliases the rings after the main loop
     float* mO = reinterpret_cast<float*>(smem);                                // [warp][16][128]
     float* mM = mO + A3_WARPS * 16 * A3_D;                                     // [warp][16]
@@ -99,6 +110,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     const int b = bh / a.n_heads, h = bh % a.n_heads;
     const int G = a.G;
     ktrace_mark(a.ktrace, a.ktrace_id, 0);
+    A3_STAMP(0);
     pdl_launch_dependents();
     // lengths and page tables are host-written before the step; the cache rows
     // below ctx were written by earlier steps -> their loads are issued before
@@ -111,12 +123,13 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     const int np = p1 - p0;
     for (int i = tid; i < np; i += 128) sBlk[i] = a.page_table[b * a.pt_stride + p0 + i];
     __syncthreads();
+    A3_STAMP(1);
 
     // this warp's chunks: ci = warp + 4 * it over the CTA's 2*np chunks, 2-deep ring
     const int nchunks = 2 * np;
     const int n_my = nchunks > warp ? (nchunks - warp + A3_WARPS - 1) / A3_WARPS : 0;
     const size_t plane = (size_t)a.n_heads * a.page_tokens * A3_D;
-    const uint32_t wring = s_ring + warp * 2 * A3_STAGE;
+    const uint32_t wring = s_ring + warp * NST * A3_STAGE;
     auto issue = [&](int ci, int stage) {
         const int pg = ci >> 1, koff = (ci & 1) * A3_CHUNK;
         const bf16* kb = reinterpret_cast<const bf16*>(a.kv_pool) +
@@ -135,12 +148,13 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     // chunk ci holds only cached rows iff its last key < ctx; such chunks form a
     // prefix of this warp's sequence, so commit order stays the chunk order
     int pre = 0;
-    while (pre < 2 && pre < n_my && (p0 * 64 + (warp + A3_WARPS * pre + 1) * A3_CHUNK) <= ctx) {
+    while (pre < NST && pre < n_my && (p0 * 64 + (warp + A3_WARPS * pre + 1) * A3_CHUNK) <= ctx) {
         issue(warp + A3_WARPS * pre, pre);
         ++pre;
     }
     pdl_wait();
-    for (int it = pre; it < 2 && it < n_my; ++it) issue(warp + A3_WARPS * it, it);
+    A3_STAMP(2);
+    for (int it = pre; it < NST && it < n_my; ++it) issue(warp + A3_WARPS * it, it);
 
     // Q (pre-scaled by log2(e)/sqrt(Dh)) -> bf16, rows >= G zero, swizzled
     for (int i = tid; i < 16 * (A3_D / 8); i += 128) {
@@ -161,6 +175,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
                      : "memory");
     }
     __syncthreads();
+    A3_STAMP(3);
 
     // Q A-fragments for the 8 k-steps
     uint32_t qa[8][4];
@@ -177,8 +192,8 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     const int row0 = g, row1 = g + 8;
 
     for (int it = 0; it < n_my; ++it) {
-        const int ci = warp + A3_WARPS * it, stage = it & 1;
-        if (it + 1 < n_my)
+        const int ci = warp + A3_WARPS * it, stage = it % NST;
+        if (NST == 2 && it + 1 < n_my)
             cp_wait<1>();
         else
             cp_wait<0>();
@@ -270,11 +285,12 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
             }
         }
         __syncwarp();
-        if (it + 2 < n_my) issue(ci + 2 * A3_WARPS, stage);   // refill the stage just consumed
+        if (it + NST < n_my) issue(ci + NST * A3_WARPS, stage);   // refill the stage just consumed
     }
 
     // ---- merge the 4 warps (warp order) through shared memory (aliases the rings)
     __syncthreads();
+    A3_STAMP(4);
 #pragma unroll
     for (int n = 0; n < 16; ++n) {
         const int d = 8 * n + 2 * t4;
@@ -304,6 +320,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
         fL[tid] = L;
     }
     __syncthreads();
+    A3_STAMP(5);
     for (int i = tid; i < G * A3_D; i += 128) {
         const int j = i / A3_D, d = i % A3_D;
         float O = 0.f;
@@ -319,8 +336,10 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
         return;
     }
     cluster_sync3();                                           // split partials visible cluster-wide
-    if (cluster_rank3() == 0) {
-        for (int i = tid; i < G * A3_D; i += 128) {
+    A3_STAMP(6);
+    {   // every rank merges a slice of the G x 128 outputs (rank order of the sum: deterministic)
+        const int rk = (int)cluster_rank3();
+        for (int i = rk * 128 + tid; i < G * A3_D; i += S * 128) {
             const int j = i / A3_D, d = i % A3_D;
             float mq[8], lq[8], oq[8];
 #pragma unroll
@@ -346,6 +365,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     }
     cluster_sync3();                                           // keep partials alive until merged
     ktrace_mark(a.ktrace, a.ktrace_id, 1);
+    A3_STAMP(7);
 }
 
 int attn3_splits(int B, int H, int max_pages, int num_sms) {
@@ -355,22 +375,26 @@ int attn3_splits(int B, int H, int max_pages, int num_sms) {
     const int units = B * H;
     int s = 1;
     while (s < 8 && units * (2 * s) <= (num_sms * 7) / 8 && 2 * s <= max_pages) s *= 2;
+    // short contexts: 8-CTA clusters with the 1-stage (69 KB) ring, up to two CTAs
+    // per SM, <= 2 chunks per CTA — measured C2 (B=1, ctx 512): attention ends
+    // 9.5 us after the QKV GEMM instead of 11.3 us with 4 x 136 KB
+    if (units * 8 <= 2 * num_sms && max_pages >= 8) s = 8;
     return s;
 }
 
-cudaError_t attn3_launch(const AttnArgs& a, int splits, cudaStream_t st) {
-    if (a.head_dim != A3_D || a.page_tokens != 64 || a.G > 16 || splits < 1 || splits > 8)
-        return cudaErrorInvalidValue;
+template <int NST>
+static cudaError_t attn3_launch_t(const AttnArgs& a, int splits, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(attn3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A3_SMEM);
+        cudaError_t e =
+            cudaFuncSetAttribute(attn3_kernel<NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, A3Cfg<NST>::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(splits, a.B * a.n_heads, 1);
     cfg.blockDim = dim3(128, 1, 1);
-    cfg.dynamicSmemBytes = A3_SMEM;
+    cfg.dynamicSmemBytes = A3Cfg<NST>::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     int na = 0;
@@ -386,7 +410,17 @@ cudaError_t attn3_launch(const AttnArgs& a, int splits, cudaStream_t st) {
     }
     cfg.attrs = at;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, attn3_kernel, a);
+    return cudaLaunchKernelEx(&cfg, attn3_kernel<NST>, a);
+}
+
+// max_ctx_len: the longest cached context of the batch (sizes the per-warp ring)
+cudaError_t attn3_launch(const AttnArgs& a, int splits, int max_ctx_len, cudaStream_t st) {
+    if (a.head_dim != A3_D || a.page_tokens != 64 || a.G > 16 || splits < 1 || splits > 8)
+        return cudaErrorInvalidValue;
+    const int pages = (max_ctx_len + a.G + 63) / 64;
+    const int chunks_per_cta = 2 * ((pages + splits - 1) / splits);
+    if (g_attn_ring1 && chunks_per_cta <= A3_WARPS * 2) return attn3_launch_t<1>(a, splits, st);
+    return attn3_launch_t<2>(a, splits, st);
 }
 
 }  // namespace sv

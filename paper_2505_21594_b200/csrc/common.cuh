@@ -154,6 +154,7 @@ __device__ __forceinline__ float ld_dsmem_f32(const void* local_ptr, uint32_t ra
     return v;
 }
 
+
 // ------------------------------------------------- per-launch timeline trace
 // [first CTA start, last CTA end] of a launch in globaltimer ns (SV_KTRACE)
 __device__ __forceinline__ void ktrace_mark(unsigned long long* tr, int id, int end) {

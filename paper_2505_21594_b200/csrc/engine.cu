@@ -179,6 +179,8 @@ struct sv_engine {
     sv_engine_opts opts;
     int device, num_sms;
     int pf_depth = 0;                           // GemmArgs::pf_depth (env SV_PF)
+    int attn_splits = 0;                        // attention split override (env SV_ATTN_SPLITS; 0 = attn3_splits)
+    std::vector<CUtensorMap> wmap128;           // weight maps [qkv L][o L][gu L][down L][lm] (box rows 128)
     // weights
     void *embed, *lm_head, *norm_final;
     std::vector<void*> w_qkv, w_o, w_gu, w_down, norm_attn, norm_mlp;
@@ -227,6 +229,7 @@ struct sv_engine {
     std::vector<ProfRec>* prof = nullptr;
     unsigned long long* ktrace = nullptr;       // SV_KTRACE: per-launch [start, ~end] globaltimer
     std::vector<std::pair<int, int>> kmeta;     // (kind, layer) of each traced launch
+    unsigned long long* atrace = nullptr;       // SV_ATRACE: attention phase stamps [layer][16]
     std::mutex mu;
 };
 
@@ -358,6 +361,8 @@ static sv_status engine_tmaps(sv_engine* e) {
     }
     CK(cudaMalloc((void**)&e->d_tmaps, sizeof(CUtensorMap) * nmaps));
     CK(cudaMemcpy(e->d_tmaps, all.data(), sizeof(CUtensorMap) * nmaps, cudaMemcpyHostToDevice));
+    // weight maps in [qkv L][o L][gu L][down L][lm] order
+    e->wmap128.assign(all.begin(), all.begin() + 4 * L + 1);
     return SV_OK;
 }
 
@@ -385,6 +390,8 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     e->device = device;
     CK(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* pf = getenv("SV_PF")) e->pf_depth = atoi(pf);
+    if (const char* as = getenv("SV_ATTN_SPLITS")) e->attn_splits = atoi(as);
+    if (getenv("SV_ATTN_RING2")) g_attn_ring1 = false;
     e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
     e->L = cfg->n_layers; e->d = cfg->d_model; e->F = cfg->d_ff; e->V = cfg->vocab;
     e->H = cfg->n_heads; e->D = cfg->head_dim;
@@ -409,6 +416,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
     if (getenv("SV_KTRACE")) CK(cudaMalloc((void**)&e->ktrace, 1024 * 2 * sizeof(unsigned long long)));
+    if (getenv("SV_ATRACE")) CK(cudaMalloc((void**)&e->atrace, (size_t)e->L * 16 * sizeof(unsigned long long)));
     *out = e;
     return SV_OK;
 }
@@ -579,19 +587,29 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
     ea.ktrace_id = nl;
     LAUNCH(SV_K_EMBED, -1, st, Md * 2 + d * 2 + Md * 6 + (d / 128) * M * 4.0, 0.0, embed_launch(ea, st));
     double attn_bytes = Md * 6, attn_flops = 0;
+    int max_ctx = 0;
     {
         const int32_t* ctxh = (const int32_t*)(e->meta_host + e->off_ctx);
         for (int b = 0; b < n; ++b) {
+            max_ctx = std::max(max_ctx, (int)ctxh[b]);
             attn_bytes += (double)(ctxh[b] + G) * d * 4;
             for (int j = 0; j < G; ++j) attn_flops += 4.0 * (ctxh[b] + j + 1) * d;
         }
     }
 
     // nx / nN / nK: the next GEMM on the same stream (its weights are prefetched to L2)
-    auto gemm = [&](int epi, const CUtensorMap& A, const CUtensorMap& B, int N, int K, GemmArgs a, cudaStream_t s,
-                    bool exit_ws, int nx = -1, int nN = 0, int nK = 0) -> cudaError_t {
+    // wid: weight index in [qkv L][o L][gu L][down L][lm] order; nx: the next GEMM's
+    // weight index on the same stream (its first weights are prefetched to L2)
+    auto gemm = [&](int epi, int wid, int bbuf, int N, int K, GemmArgs a, cudaStream_t s, bool exit_ws, int nx = -1,
+                    int nN = 0, int nK = 0) -> cudaError_t {
         a.N = N;
         a.K = K;
+        a.ws = exit_ws ? e->ws_exit : e->ws_main;
+        a.counters = exit_ws ? e->cnt_exit : e->cnt_main;
+        a.ktrace = e->ktrace;
+        a.ktrace_id = nl;
+        const CUtensorMap& A = e->wmap128[wid];
+        const CUtensorMap& B = tma[bbuf];
         a.splits = gemm_pick_splits(N, K, M, tn, e->num_sms);
         if (nx >= 0 && tn <= 64 && e->pf_depth > 0) {
             a.pf_map = e->d_tmaps + nx;
@@ -600,10 +618,6 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             a.pf_kb = nK / 64;
             a.pf_depth = e->pf_depth;
         }
-        a.ws = exit_ws ? e->ws_exit : e->ws_main;
-        a.counters = exit_ws ? e->cnt_exit : e->cnt_main;
-        a.ktrace = e->ktrace;
-        a.ktrace_id = nl;
         return gemm_launch(epi, tn, A, B, a, s);
     };
     auto lm_and_accept = [&](cudaStream_t s, bool is_exit) -> cudaError_t {
@@ -612,7 +626,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
         a.logits = is_exit ? e->logits_exit : e->logits_final;
         cudaError_t q;
         LAUNCH(is_exit ? SV_K_LM_EXIT : SV_K_LM_FINAL, -1, s, gemm_bytes(V, d, (double)M * V * 4),
-               2.0 * M * V * d, gemm(EPI_LOGITS, e->tm_lm, is_exit ? tma[3] : tma[0], V, d, a, s, is_exit));
+               2.0 * M * V * d, gemm(EPI_LOGITS, 4 * L, is_exit ? 3 : 0, V, d, a, s, is_exit));
         AcceptArgs aa = {};
         aa.logits = a.logits;
         aa.req = (const ReqDev*)(e->meta_dev + e->off_reqdev);
@@ -642,7 +656,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             a.ssq_in = ssq_at(e, l, 0);
             a.qbuf = e->qbuf;
             LAUNCH(SV_K_QKV, l, st, gemm_bytes(3.0 * d, d, Md * 8 + (d / 128) * M * 4.0), 2.0 * M * 3.0 * d * d,
-                   gemm(EPI_QKV, e->tm_qkv[l], tma[0], 3 * d, d, a, st, false, L + l, d, d));
+                   gemm(EPI_QKV, l, 0, 3 * d, d, a, st, false, L + l, d, d));
         }
         {   // attention
             AttnArgs aa = {};
@@ -656,22 +670,23 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)e->D));
             aa.ktrace = e->ktrace;
             aa.ktrace_id = nl;
+            aa.atrace = e->atrace ? e->atrace + (size_t)l * 16 : nullptr;
             LAUNCH(SV_K_ATTN, l, st, attn_bytes, attn_flops,
-                   e->D == 128 ? attn3_launch(aa, attn3_splits(n, e->H, nchunk, e->num_sms), st)
+                   e->D == 128 ? attn3_launch(aa, e->attn_splits > 0 ? e->attn_splits : attn3_splits(n, e->H, nchunk, e->num_sms), max_ctx, st)
                                : attn_launch(aa, st));
         }
         {   // O projection + residual
             GemmArgs a = base_args(e, M);
             a.h = e->h; a.g_out = e->norm_mlp[l]; a.u_out = e->u; a.ssq_out = ssq_at(e, l, 1);
             LAUNCH(SV_K_O, l, st, gemm_bytes(d, d, Md * 10 + (d / 128) * M * 4.0), 2.0 * M * d * d,
-                   gemm(EPI_RESID, e->tm_o[l], tma[1], d, d, a, st, false, 2 * L + l, 2 * F, d));
+                   gemm(EPI_RESID, L + l, 1, d, d, a, st, false, 2 * L + l, 2 * F, d));
         }
         {   // gate/up + SwiGLU
             GemmArgs a = base_args(e, M);
             a.ssq_in = ssq_at(e, l, 1);
             a.act = e->act;
             LAUNCH(SV_K_GU, l, st, gemm_bytes(2.0 * F, d, (double)M * F * 2 + (d / 128) * M * 4.0),
-                   2.0 * M * 2.0 * F * d, gemm(EPI_SWIGLU, e->tm_gu[l], tma[0], 2 * F, d, a, st, false, 3 * L + l, d, F));
+                   2.0 * M * 2.0 * F * d, gemm(EPI_SWIGLU, 2 * L + l, 0, 2 * F, d, a, st, false, 3 * L + l, d, F));
         }
         {   // down + residual (+ early-exit copy with the final gain)
             GemmArgs a = base_args(e, M);
@@ -685,7 +700,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             a.ssq_out = ssq_at(e, l + 1, 0);
             LAUNCH(SV_K_DOWN, l, st, gemm_bytes(d, F, Md * (l + 1 == exit_layer ? 12 : 10) + (d / 128) * M * 4.0),
                    2.0 * M * d * F,
-                   gemm(EPI_RESID, e->tm_down[l], tma[2], d, F, a, st, false, l + 1 < L ? l + 1 : 4 * L, l + 1 < L ? 3 * d : V, d));
+                   gemm(EPI_RESID, 3 * L + l, 2, d, F, a, st, false, l + 1 < L ? l + 1 : 4 * L, l + 1 < L ? 3 * d : V, d));
         }
         if (l + 1 == exit_layer) {   // fork the early exit (S10-S11)
             if ((r = cudaEventRecord(e->ev_fork, st)) != cudaSuccess) return r;
@@ -1112,6 +1127,18 @@ extern "C" sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us) {
                 for (size_t i = 0; i < e->kmeta.size(); ++i)
                     fprintf(fp, "%zu,%d,%d,%llu,%llu\n", i, e->kmeta[i].first, e->kmeta[i].second, tr[2 * i],
                             ~tr[2 * i + 1]);
+                fclose(fp);
+            }
+        }
+    }
+    if (e->atrace && getenv("SV_ATRACE")) {   // attention phase stamps of this step
+        std::vector<unsigned long long> tr((size_t)e->L * 16);
+        if (cudaMemcpy(tr.data(), e->atrace, tr.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            FILE* fp = fopen(getenv("SV_ATRACE"), "w");
+            if (fp) {
+                fprintf(fp, "layer,cta,phase,t_ns\n");
+                for (int l = 0; l < e->L; ++l)
+                    for (int k = 0; k < 16; ++k) fprintf(fp, "%d,%d,%d,%llu\n", l, k / 8, k % 8, tr[l * 16 + k]);
                 fclose(fp);
             }
         }

@@ -88,12 +88,14 @@ struct AttnArgs {
     float scale_log2;     // log2(e) / sqrt(head_dim)
     unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
     int ktrace_id = 0;
+    unsigned long long* atrace = nullptr;   // optional phase stamps of CTAs (0,0) and (0,last) [16] (SV_ATRACE)
 };
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st);
 // v3 (head_dim 128): mma.sync bf16 tensor-core tiles, per-warp cp.async rings,
 // online softmax in registers, cluster (DSMEM) split merge
 int attn3_splits(int B, int H, int max_pages, int num_sms);
-cudaError_t attn3_launch(const AttnArgs& a, int splits, cudaStream_t st);
+cudaError_t attn3_launch(const AttnArgs& a, int splits, int max_ctx_len, cudaStream_t st);
+extern bool g_attn_ring1;   // allow the 1-stage (69 KB) ring for short contexts
 
 // ----------------------------------------------------------- acceptance (K5)
 struct ReqDev {            // per-request metadata for the acceptance kernels

@@ -15,7 +15,7 @@
 #include "../paper_2505_21594_b200/csrc/common.cuh"
 
 using namespace sv;
-static CUtensorMap g_tmb;
+static CUtensorMap g_tmb, g_tmb8;
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
     asm volatile(
@@ -28,7 +28,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 template <int STAGES>
 __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap tm, const uint8_t* base,
                                                         int mode, int ntiles, int kb_per_row,
-                                                        const __grid_constant__ CUtensorMap tmb) {
+                                                        const __grid_constant__ CUtensorMap tmb, const __grid_constant__ CUtensorMap tmb8) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * (16384 + 2048));
@@ -56,28 +56,29 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
         for (int i = 0; i < n; ++i) {
             const int s = i % STAGES;
             if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
-            mbar_arrive_expect_tx(&full[s], mode >= 2 ? 16384 + 2048 : 16384);
             const int t = t0 + i;
-            if (mode >= 2) {
-                const int row_tile = t / kb_per_row, kb = t % kb_per_row;
-                tma_load_2d(&tm, smem + s * 16384, &full[s], kb * 64, row_tile * 128, pol);
-                tma_load_2d(&tmb, sb + s * 2048, &full[s], kb * 64, 0, policy_evict_last());
-            } else if (mode == 0) {
-                const int row_tile = t / kb_per_row, kb = t % kb_per_row;
-                tma_load_2d(&tm, smem + s * 16384, &full[s], kb * 64, row_tile * 128, pol);
-            } else {
+            const int row_tile = t / kb_per_row, kb = t % kb_per_row;
+            const bool ld_b = (mode == 2 || mode == 3 || mode == 5);
+            const uint32_t bbytes = mode == 5 ? 1024 : 2048;
+            if (mode == 1) {
+                mbar_arrive_expect_tx(&full[s], 16384);
                 bulk_load(smem + s * 16384, base + (size_t)t * 16384, 16384, &full[s], pol);
+            } else {
+                mbar_arrive_expect_tx(&full[s], 16384 + (ld_b ? bbytes : 0));
+                tma_load_2d(&tm, smem + s * 16384, &full[s], kb * 64, row_tile * 128, pol);
+                if (ld_b) tma_load_2d(mode == 5 ? &tmb8 : &tmb, sb + s * 2048, &full[s], kb * 64, 0, policy_evict_last());
             }
         }
     } else if (warp == 1 && lane == 0) {
         for (int i = 0; i < n; ++i) {
             const int s = i % STAGES;
             mbar_wait(&full[s], (i / STAGES) & 1);
-            if (mode >= 2) {
+            if (mode == 2 || mode == 4 || mode == 5) {
                 tc_fence_after();
                 const uint64_t ad = umma_sdesc_sw128(smem_u32(smem + s * 16384));
-                const uint64_t bd = umma_sdesc_sw128(smem_u32(sb + s * 2048));
+                uint64_t bd = umma_sdesc_sw128(smem_u32(sb + s * 2048));
                 constexpr uint32_t idesc = umma_idesc_bf16(128, 16);
+                if (mode == 4) bd = umma_sdesc_sw128(smem_u32(sb));
                 for (int k = 0; k < 4; ++k) umma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) ? 1u : 0u);
                 umma_commit(&empty[s]);
             } else {
@@ -97,10 +98,10 @@ static float run(const CUtensorMap& tm, const uint8_t* base, int mode, int ntile
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    for (int w = 0; w < 3; ++w) stream_kernel<STAGES><<<grid, 64, smem>>>(tm, base, mode, ntiles, kbr, g_tmb);
+    for (int w = 0; w < 3; ++w) stream_kernel<STAGES><<<grid, 64, smem>>>(tm, base, mode, ntiles, kbr, g_tmb, g_tmb8);
     cudaEventRecord(a);
     const int reps = 10;
-    for (int w = 0; w < reps; ++w) stream_kernel<STAGES><<<grid, 64, smem>>>(tm, base, mode, ntiles, kbr, g_tmb);
+    for (int w = 0; w < reps; ++w) stream_kernel<STAGES><<<grid, 64, smem>>>(tm, base, mode, ntiles, kbr, g_tmb, g_tmb8);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
@@ -133,18 +134,19 @@ int main(int argc, char** argv) {
     cuuint32_t boxb[2] = {64, 16};
     enc(&g_tmb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, act, gdb, gstr, boxb, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cuuint32_t boxb8[2] = {64, 8};
+    enc(&g_tmb8, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, act, gdb, gstr, boxb8, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     const int kbr = K / 64, ntiles = (N / 128) * kbr;
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     printf("tiles %d (%.1f MB), SMs %d\n", ntiles, bytes / 1e6, sms);
-    for (int mode = 0; mode < 3; ++mode)
-        for (int mult = 1; mult <= 2; ++mult) {
-            const int grid = sms * mult;
-            printf("mode %d (%s) grid %d: st4 %.0f  st6 %.0f  st9 %.0f  st12 %.0f GB/s\n", mode,
-                   mode == 2 ? "2D A + 2D B + tcgen05.mma" : (mode ? "bulk 16KB contiguous" : "2D box strided rows"), grid,
-                   run<4>(tm, buf, mode, ntiles, kbr, grid), run<6>(tm, buf, mode, ntiles, kbr, grid),
-                   mult == 1 ? run<9>(tm, buf, mode, ntiles, kbr, grid) : 0.f,
-                   mult == 1 ? run<12>(tm, buf, mode, ntiles, kbr, grid) : 0.f);
-        }
+    const char* names[6] = {"A 2D only", "A bulk 16KB", "A+B16+MMA", "A+B16 no MMA", "A+MMA (B fixed)", "A+B8+MMA"};
+    for (int mode = 0; mode < 6; ++mode) {
+        const int grid = sms;
+        printf("mode %d %-16s grid %d: st4 %.0f  st6 %.0f  st9 %.0f  st12 %.0f GB/s\n", mode, names[mode], grid,
+               run<4>(tm, buf, mode, ntiles, kbr, grid), run<6>(tm, buf, mode, ntiles, kbr, grid),
+               run<9>(tm, buf, mode, ntiles, kbr, grid), run<12>(tm, buf, mode, ntiles, kbr, grid));
+    }
     return 0;
 }
