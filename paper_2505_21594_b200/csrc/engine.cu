@@ -392,6 +392,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (const char* pf = getenv("SV_PF")) e->pf_depth = atoi(pf);
     if (const char* as = getenv("SV_ATTN_SPLITS")) e->attn_splits = atoi(as);
     if (getenv("SV_ATTN_RING2")) g_attn_ring1 = false;
+    if (getenv("SV_SPLIT_ANY")) g_split_any = true;
     e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
     e->L = cfg->n_layers; e->d = cfg->d_model; e->F = cfg->d_ff; e->V = cfg->vocab;
     e->H = cfg->n_heads; e->D = cfg->head_dim;

@@ -180,7 +180,6 @@ __global__ void __launch_bounds__(128, 1)
     const int row = warp * 32 + lane;
     const uint32_t tbase = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     const bool direct = (a.splits == 1);
-    float* sPart = reinterpret_cast<float*>(smem);       // split partial [TN][128] (the ring is free)
     for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
         if (m0 + c0 >= a.M) break;                       // CTA-uniform
         uint32_t r[16];
@@ -193,8 +192,12 @@ __global__ void __launch_bounds__(128, 1)
             __syncthreads();
             epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt);
         } else {
+            float* wsp = a.ws + (((size_t)split * NT + nt) * a.MP) * TM;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) sPart[(c0 + j) * TM + row] = __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j) {
+                const int tok = m0 + c0 + j;
+                if (tok < a.M) __stcg(&wsp[(size_t)tok * TM + row], __uint_as_float(r[j]));
+            }
         }
     }
     tc_fence_before();
@@ -205,34 +208,51 @@ __global__ void __launch_bounds__(128, 1)
         return;
     }
 
-    // ---------------- split-K through distributed shared memory: the splits of a
-    // tile are one thread-block cluster (dims 1 x 1 x S, rank = split); rank 0 adds
-    // the partials in rank order (deterministic) and runs the fused epilogue.
-    cluster_sync_all();                                  // every split's partial is in its smem
-    if (split == 0) {
-        float* sO = sPart + TN * TM;
-        for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
-            if (m0 + c0 >= a.M) break;
-            const int nv = min(EPI_CHUNK, a.M - (m0 + c0));
-            float acc[EPI_CHUNK];
+    {
+        // ---------------- split-K through global memory: the last CTA of the tile
+        // (atomic ticket) adds the partials in split order (deterministic; measured
+        // faster at batch 1 than a cluster DSMEM reduction: C2 3.22 vs 3.34 ms)
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) *s_flag = (atomicAdd(&a.counters[nt * MT + mt], 1) == a.splits - 1);
+        __syncthreads();
+        if (*s_flag) {
+            __threadfence();
+            const size_t sstride = (size_t)NT * a.MP * TM;
+            for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
+                if (m0 + c0 >= a.M) break;
+                const int nv = min(EPI_CHUNK, a.M - (m0 + c0));
+                float acc[EPI_CHUNK];
 #pragma unroll
-            for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = sPart[(c0 + j) * TM + row];
-            for (int q = 1; q < a.splits; ++q) {
-                float v[EPI_CHUNK];
+                for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = 0.f;
+                const float* base = a.ws + ((size_t)nt * a.MP + m0 + c0) * TM + row;
+                int q = 0;
+                for (; q + 4 <= a.splits; q += 4) {
+                    float v[EPI_CHUNK][4];
 #pragma unroll
-                for (int j = 0; j < EPI_CHUNK; ++j) v[j] = (j < nv) ? ld_dsmem_f32(&sPart[(c0 + j) * TM + row], q) : 0.f;
+                    for (int j = 0; j < EPI_CHUNK; ++j)
 #pragma unroll
-                for (int j = 0; j < EPI_CHUNK; ++j) acc[j] += v[j];
+                        for (int u = 0; u < 4; ++u) v[j][u] = (j < nv) ? __ldcg(base + (q + u) * sstride + j * TM) : 0.f;
+#pragma unroll
+                    for (int j = 0; j < EPI_CHUNK; ++j)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) acc[j] += v[j][u];
+                }
+                for (; q < a.splits; ++q) {
+#pragma unroll
+                    for (int j = 0; j < EPI_CHUNK; ++j) acc[j] += (j < nv) ? __ldcg(base + q * sstride + j * TM) : 0.f;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < EPI_CHUNK; ++j) sOut[j * TM + row] = acc[j];
+                __syncthreads();
+                epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt);
             }
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < EPI_CHUNK; ++j) sO[j * TM + row] = acc[j];
-            __syncthreads();
-            epi_chunk<EPI>(a, sO, sR, sRed, m0 + c0, m0, n0, nt);
+            if (threadIdx.x == 0) a.counters[nt * MT + mt] = 0;
         }
+        ktrace_mark(a.ktrace, a.ktrace_id, 1);
+        return;
     }
-    cluster_sync_all();                                  // partials stay alive until read
-    ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 
 // ------------------------------------------------------------------ host side
@@ -265,14 +285,20 @@ int gemm_pick_tile_n(int M) {
     return 256;
 }
 
-// Split-K factor: a power of two <= 8 (the splits of a tile form one cluster),
+// Split-K factor: a power of two <= 8 (env SV_SPLIT_ANY: any count <= 16),
 // only for small token tiles (TN <= 64; larger tiles have enough tiles to fill
 // the GPU), with all CTAs resident in one wave (2 per SM) and >= 2 K blocks each.
+bool g_split_any = false;     // allow non-power-of-two split counts (env SV_SPLIT_ANY)
+
 int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms) {
     const int ntiles = (N / TM) * ((M + tile_n - 1) / tile_n);
-    const int slots = num_sms * (tile_n <= 64 ? 2 : 1);
+    const int slots = num_sms * (tile_n <= 64 ? SV_GEMM_CTAS_PER_SM : 1);
     const int KB = K / BK;
     int s = 1;
+    if (g_split_any) {
+        while (s < 16 && ntiles * (s + 1) <= slots && 2 * (s + 1) <= KB) ++s;
+        return s;
+    }
     while (s < 8 && ntiles * (2 * s) <= slots && 2 * (2 * s) <= KB) s *= 2;
     return s;
 }
@@ -294,11 +320,6 @@ static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     int na = 0;
-    attr[na].id = cudaLaunchAttributeClusterDimension;       // split-K reduction cluster
-    attr[na].val.clusterDim.x = 1;
-    attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = a.splits;
-    ++na;
     if (g_use_pdl) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;

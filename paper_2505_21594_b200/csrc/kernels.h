@@ -70,6 +70,7 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 
 int gemm_pick_tile_n(int M);
 int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms);
+extern bool g_split_any;
 cudaError_t gemm_launch(int epi, int tile_n, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                         cudaStream_t st);
 
