@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4", "C5"])
     ap.add_argument("--gamma", type=int, default=4)
     ap.add_argument("--exit-layer", type=int, default=16)
+    ap.add_argument("--all-exits", action="store_true",
+                    help="NEXT-1: an early exit after every layer 1..L-1, streamed (overrides --exit-layer)")
     ap.add_argument("--alpha", type=float, default=0.825)
     ap.add_argument("--batch", type=int, default=None, help="requests per GPU (default: per config)")
     ap.add_argument("--ctx", type=int, default=None)
@@ -308,6 +310,9 @@ def run_ours(args):
     per, total, ctx, scaling = workload(args, world)
     gamma, exit_layer = args.gamma, args.exit_layer
     mc = llama2_7b()
+    exit_layers = list(range(1, mc.n_layers)) if args.all_exits else []
+    if exit_layers:
+        exit_layer = 0
     W = sv.Weights(mc, seed=1, device=local)
     blocks_per = (ctx + gamma + 1 + 63) // 64
     eng = sv.Engine(mc, W, max_batch=per, max_gamma=gamma, kv_blocks=per * blocks_per, device=local)
@@ -336,9 +341,14 @@ def run_ours(args):
             s.rewind(ctx)
         reqs = [sv.Request(s, rounds.next(s), pend[b], x[b], q_host[k][b] if host_probs else q_dev[k][b])
                 for b, s in enumerate(sessions)]
-        t = eng.submit(reqs, exit_layer=exit_layer, stream=stream)
-        if exit_layer:
-            t.wait_early()
+        if exit_layers:
+            t = eng.submit_exits(reqs, exit_layers, stream=stream)
+            for k in range(len(exit_layers)):       # streamed: each exit as soon as it lands
+                t.wait_exit(k)
+        else:
+            t = eng.submit(reqs, exit_layer=exit_layer, stream=stream)
+            if exit_layer:
+                t.wait_early()
         f = t.wait_final()
         t.release()
         return sum(r.accepted + 1 for r in f), f
@@ -388,7 +398,7 @@ def run_ours(args):
     for s in sessions:
         s.rewind(ctx)
     preqs = [sv.Request(s, rounds.next(s), pend[b], xs[0][b], q_dev[0][b]) for b, s in enumerate(sessions)]
-    _, recs = eng.profile_step(preqs, exit_layer=exit_layer)
+    _, recs = eng.profile_step(preqs, exit_layer=exit_layer if not exit_layers else exit_layers[len(exit_layers) // 2])
 
     # gather counters over ranks (the only collective)
     allv = gather_counters([tokens, elapsed, e2e_tok, e2e_el], device="cuda")
@@ -423,6 +433,9 @@ def run_ours(args):
     achieved = g_bytes / (g_ms / 1e3) / 1e9
     tr = ncu_traffic(tr_key)
     step_bytes = sum(r["bytes"] for r in recs)
+    if exit_layers:   # the profiled step ran one exit; the timed steps ran len(exit_layers)
+        step_bytes += (len(exit_layers) - 1) * sum(r["bytes"] for r in recs
+                                                   if r["kind"] in ("gemm_lm_exit", "accept_exit"))
     roofline = {"bound": "hbm", "kernel": dom_name,
                 "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                 "traffic": tr, "peak_source": peak_src,
@@ -453,9 +466,12 @@ def run_ours(args):
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random-init Llama2-7B-shape weights, synthetic KV, calibrated draft distributions)",
             "config": {"workload": f"{args.config}: Llama2-7B shape (32 layers, d 4096, V 32000), "
-                                   f"{per} request(s)/GPU, ctx {ctx}, gamma {gamma}, early exit at layer "
-                                   f"{exit_layer}, stochastic acceptance, alpha {args.alpha}",
-                       "global_batch": total, "seq_len": ctx, "gamma": gamma, "exit_layer": exit_layer,
+                                   f"{per} request(s)/GPU, ctx {ctx}, gamma {gamma}, "
+                                   + (f"early exits after layers 1..{mc.n_layers - 1} (streamed)" if exit_layers
+                                      else f"early exit at layer {exit_layer}")
+                                   + f", stochastic acceptance, alpha {args.alpha}",
+                       "global_batch": total, "seq_len": ctx, "gamma": gamma,
+                       "exit_layer": exit_layers if exit_layers else exit_layer,
                        "engine": "fused persistent step kernel" if eng.fused else "per-op kernels + CUDA graph + PDL",
                        "parallelism": f"requests sharded over {world} GPU(s), weights replicated",
                        "l2": "inputs larger than L2 (13.5 GB of weights streamed per step)"},

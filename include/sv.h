@@ -180,8 +180,31 @@ typedef struct {
 SV_API sv_status sv_verify_submit(sv_engine* e, const sv_verify_req* reqs, int32_t n, int32_t exit_layer,
                            sv_exit_result* early, sv_exit_result* final_, void* stream,
                            sv_ticket** out);
-SV_API sv_status sv_wait_early(sv_ticket* t, int64_t timeout_us);
+SV_API sv_status sv_wait_early(sv_ticket* t, int64_t timeout_us);  /* all early exits of the ticket */
 SV_API sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us);   /* KV already rolled back */
+
+/* All-exits streaming verify (Alg-S lines 1103-1106,
+ * the server verifies the draft at every exit and pushes each
+ * exit's result with its score as soon as that exit is computed; T-eeft,
+ * 31 exits for Llama2-7B).
+ * exit_layers: host [n_exits], strictly ascending, each in 1..n_layers (n_layers
+ * itself = an exit at the final layer, bitwise equal to the final result);
+ * n_exits <= n_layers <= 64; the fused engine accepts n_exits <= 1.  Every exit
+ * uses the same Philox counters as the final exit (R10) and none of
+ * them changes the session (KV, length).
+ * early: host [n_exits][n]; row k is valid after sv_wait_exit(t, k) (or after
+ * sv_wait_early / sv_wait_final).  Errors: SV_E_INVALID for a bad list, otherwise
+ * as sv_verify_submit (which is this call with {exit_layer} or no exit). */
+SV_API sv_status sv_verify_submit_exits(sv_engine* e, const sv_verify_req* reqs, int32_t n,
+                                        const int32_t* exit_layers, int32_t n_exits, sv_exit_result* early,
+                                        sv_exit_result* final_, void* stream, sv_ticket** out);
+/* Block until exit k (index into the submit's exit_layers) has been delivered to
+ * the host (mapped-memory flag written by the device after that exit's results),
+ * then copy its [n] results into early[k][.].  SV_E_TIMEOUT after timeout_us >= 0. */
+SV_API sv_status sv_wait_exit(sv_ticket* t, int32_t k, int64_t timeout_us);
+/* Non-blocking: number of exits (a prefix of exit_layers, in layer order) whose
+ * results have reached host memory. */
+SV_API sv_status sv_exits_ready(sv_ticket* t, int32_t* n_ready);
 SV_API sv_status sv_ticket_release(sv_ticket* t);
 
 /* The north star's synchronous form: verify(draft_tokens, draft_probs, kv) ->

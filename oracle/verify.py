@@ -3,7 +3,9 @@
 Alg-S Listener: verify the draft at every exit, push the
 early-exit results with their score, send the final result flagged final.
 This oracle runs one early exit l_e plus the final exit (the north star's
-configuration; all-exits is its repetition).
+configuration), or any list of exits (`exit_layers`: the all-exits streaming
+verify of Alg-S; each exit is the LM head on h^(l),
+PAPER.md:101-102, accepted with the same counters as the final exit).
 
 The query block is [pending, x_1..x_gamma] at positions ctx..ctx+gamma
 (R15).  After the final acceptance the cache is rolled back to
@@ -18,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import accept as acc
-from .model import KVCache, Model, forward
+from .model import KVCache, Model, forward, lm_head
 
 
 @dataclass
@@ -36,10 +38,11 @@ class StepOut:
     final_logits: np.ndarray
     exit_logits: np.ndarray
     new_len: int
+    exits: list = None            # [(layer, Result, logits)] for exit_layers
 
 
 def verify_step(model: Model, sess: Session, round_id: int, pending: int, drafts,
-                probs=None, exit_layer: int = 0) -> StepOut:
+                probs=None, exit_layer: int = 0, exit_layers=()) -> StepOut:
     cfg = model.cfg
     drafts = [int(x) for x in drafts]
     gamma = len(drafts)
@@ -50,15 +53,19 @@ def verify_step(model: Model, sess: Session, round_id: int, pending: int, drafts
         return StepOut(bad, bad, None, None, sess.cache.length)
     ctx = sess.cache.length
     block = np.array([pending] + drafts, dtype=np.int64)
-    z, ze, _ = forward(model, sess.cache, block, exit_layer)
+    z, ze, hs = forward(model, sess.cache, block, exit_layer)
     kw = dict(seed=sess.philox_seed, session_id=sess.session_id, round_id=round_id)
     q = None if probs is None else np.asarray(probs, dtype=np.float64)
     final = acc.accept(z, drafts, q, **kw)
     early = acc.accept(ze, drafts, q, **kw) if ze is not None else None
+    exits = []
+    for le in exit_layers:                            # h^(le) = hs[le] (output of layer le)
+        zl = lm_head(model, hs[le])
+        exits.append((le, acc.accept(zl, drafts, q, **kw), zl))
     if final.status != acc.OK:
         sess.cache.truncate(ctx)                      # protocol error: KV not advanced
-        return StepOut(final, early, z, ze, ctx)
+        return StepOut(final, early, z, ze, ctx, exits)
     new_len = ctx + 1 + final.accepted
     sess.cache.truncate(new_len)                      # S14 rollback
     sess.last_round = round_id
-    return StepOut(final, early, z, ze, new_len)
+    return StepOut(final, early, z, ze, new_len, exits)

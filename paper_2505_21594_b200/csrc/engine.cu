@@ -150,9 +150,11 @@ struct sv_session {
 };
 
 struct StepKey {
-    int n, gamma, exit_layer, nchunk;
+    int n, gamma;
+    uint64_t exit_mask;   // bit l-1 set: early exit after decoder layer l
+    int nchunk;
     bool operator<(const StepKey& o) const {
-        return std::tie(n, gamma, exit_layer, nchunk) < std::tie(o.n, o.gamma, o.exit_layer, o.nchunk);
+        return std::tie(n, gamma, exit_mask, nchunk) < std::tie(o.n, o.gamma, o.exit_mask, o.nchunk);
     }
 };
 
@@ -166,11 +168,12 @@ struct sv_ticket {
     std::vector<int32_t> ctx;
     sv_exit_result* early;
     sv_exit_result* final_;
-    int exit_layer;
+    std::vector<int> exits;                      // early-exit layers, ascending (slot k = exits[k])
+    std::vector<bool> exit_done;
     uint64_t seq;
     int nb = 0, gamma = 0;
     bool has_gpu;
-    bool early_done = false, final_done = false;
+    bool final_done = false;
     cudaEvent_t ev_done;
 };
 
@@ -249,7 +252,7 @@ static sv_status engine_alloc(sv_engine* e) {
     CK(dalloc((void**)&e->logits_exit, (size_t)MP * V * 4));
     CK(dalloc((void**)&e->logits_final, (size_t)MP * V * 4));
     CK(dalloc((void**)&e->u, (size_t)MP * d * 2));
-    CK(dalloc((void**)&e->u_exit, (size_t)MP * d * 2));
+    CK(dalloc((void**)&e->u_exit, (size_t)e->L * MP * d * 2));   // one slot per exit of a step
     CK(dalloc((void**)&e->attn_out, (size_t)MP * d * 2));
     CK(dalloc((void**)&e->act, (size_t)MP * F * 2));
     // split-K workspace: the largest splits * tiles * MP * 128 over all GEMMs and row counts
@@ -312,10 +315,10 @@ static sv_status engine_alloc(sv_engine* e) {
     CK(dalloc((void**)&e->meta_dev, off));
     CK(cudaMallocHost((void**)&e->meta_host, off));
     memset(e->meta_host, 0, off);
-    CK(cudaHostAlloc((void**)&e->mb_exit, (size_t)B * sizeof(sv_exit_result), cudaHostAllocMapped));
+    CK(cudaHostAlloc((void**)&e->mb_exit, (size_t)e->L * B * sizeof(sv_exit_result), cudaHostAllocMapped));
     CK(cudaMallocHost((void**)&e->mb_final, (size_t)B * sizeof(sv_exit_result)));
-    CK(cudaHostAlloc((void**)&e->mb_flag, 64, cudaHostAllocMapped));
-    *e->mb_flag = 0;
+    CK(cudaHostAlloc((void**)&e->mb_flag, (size_t)std::max(8, e->L) * 8, cudaHostAllocMapped));
+    for (int k = 0; k < e->L; ++k) e->mb_flag[k] = 0;
     CK(cudaHostGetDevicePointer((void**)&e->mb_exit_dev, e->mb_exit, 0));
     CK(cudaHostGetDevicePointer((void**)&e->mb_flag_dev, (void*)e->mb_flag, 0));
     return SV_OK;
@@ -336,7 +339,7 @@ static sv_status engine_tmaps(sv_engine* e) {
         if (tn > e->MP) continue;
         std::vector<CUtensorMap> m(4);
         if (!make_tmap_bf16(&m[0], e->u, e->MP, d, tn) || !make_tmap_bf16(&m[1], e->attn_out, e->MP, d, tn) ||
-            !make_tmap_bf16(&m[2], e->act, e->MP, F, tn) || !make_tmap_bf16(&m[3], e->u_exit, e->MP, d, tn))
+            !make_tmap_bf16(&m[2], e->act, e->MP, F, tn) || !make_tmap_bf16(&m[3], e->u_exit, (uint64_t)e->L * e->MP, d, tn))
             return fail(SV_E_DEVICE, "tensor map (activations)");
         e->tm_act[tn] = m;
     }
@@ -540,10 +543,18 @@ static float* ssq_at(sv_engine* e, int layer, int which) {   // norm point (laye
 static cudaError_t issue_fused(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk,
                                int* launches);
 
+static int mask_single_exit(uint64_t mask) {   // the exit layer of a one-exit mask, 0 if none
+    for (int l = 1; l <= 64; ++l)
+        if (mask & (1ull << (l - 1))) return l;
+    return 0;
+}
+
 // Issues every kernel / copy of one step on (main, exit) streams; returns launch count.
-static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk,
+// exit_mask: bit l-1 = early exit after decoder layer l; the k-th exit (ascending)
+// uses u_exit slot k, mailbox rows [k][B] and flag k (streamed as each completes).
+static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, uint64_t exit_mask, int nchunk,
                               int* launches) {
-    if (e->opts.fused) return issue_fused(e, st, n, gamma, exit_layer, nchunk, launches);
+    if (e->opts.fused) return issue_fused(e, st, n, gamma, mask_single_exit(exit_mask), nchunk, launches);
     const int G = gamma + 1, M = n * G, d = e->d, F = e->F, V = e->V, L = e->L;
     const int tn = gemm_pick_tile_n(M);
     const auto& tma = e->tm_act[tn];   // {u, attn_out, act, u_exit}
@@ -621,9 +632,10 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
         }
         return gemm_launch(epi, tn, A, B, a, s);
     };
-    auto lm_and_accept = [&](cudaStream_t s, bool is_exit) -> cudaError_t {
+    auto lm_and_accept = [&](cudaStream_t s, bool is_exit, int exit_layer, int slot) -> cudaError_t {
         GemmArgs a = base_args(e, M);
         a.ssq_in = ssq_at(e, is_exit ? exit_layer : L, 0);
+        a.b_row0 = is_exit ? slot * e->MP : 0;
         a.logits = is_exit ? e->logits_exit : e->logits_final;
         cudaError_t q;
         LAUNCH(is_exit ? SV_K_LM_EXIT : SV_K_LM_FINAL, -1, s, gemm_bytes(V, d, (double)M * V * 4),
@@ -650,7 +662,10 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
         return cudaSuccess;
     };
 
+    const int n_exits = __builtin_popcountll(exit_mask);
+    int exit_k = 0;
     for (int l = 0; l < L; ++l) {
+        const bool is_exit_l = (exit_mask >> l) & 1;   // exit after layer l + 1
         {   // QKV + RoPE + KV append
             GemmArgs a = base_args(e, M);
             a.layer = l;
@@ -694,33 +709,35 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, i
             a.h = e->h;
             a.g_out = (l + 1 < L) ? e->norm_attn[l + 1] : e->norm_final;
             a.u_out = e->u;
-            if (l + 1 == exit_layer) {
+            if (is_exit_l) {
                 a.g_out2 = e->norm_final;
-                a.u_out2 = e->u_exit;
+                a.u_out2 = e->u_exit + (size_t)exit_k * e->MP * d;
             }
             a.ssq_out = ssq_at(e, l + 1, 0);
-            LAUNCH(SV_K_DOWN, l, st, gemm_bytes(d, F, Md * (l + 1 == exit_layer ? 12 : 10) + (d / 128) * M * 4.0),
+            LAUNCH(SV_K_DOWN, l, st, gemm_bytes(d, F, Md * (is_exit_l ? 12 : 10) + (d / 128) * M * 4.0),
                    2.0 * M * d * F,
                    gemm(EPI_RESID, 3 * L + l, 2, d, F, a, st, false, l + 1 < L ? l + 1 : 4 * L, l + 1 < L ? 3 * d : V, d));
         }
-        if (l + 1 == exit_layer) {   // fork the early exit (S10-S11)
+        if (is_exit_l) {   // fork early exit k (S10-S11), streamed to mailbox row k
             if ((r = cudaEventRecord(e->ev_fork, st)) != cudaSuccess) return r;
             if ((r = cudaStreamWaitEvent(e->s_exit, e->ev_fork, 0)) != cudaSuccess) return r;
-            if ((r = lm_and_accept(e->s_exit, true)) != cudaSuccess) return r;
-            if ((r = cudaMemcpyAsync(e->mb_exit, e->res_exit_dev, (size_t)n * sizeof(sv_exit_result),
+            if ((r = lm_and_accept(e->s_exit, true, l + 1, exit_k)) != cudaSuccess) return r;
+            if ((r = cudaMemcpyAsync(e->mb_exit + (size_t)exit_k * e->opts.max_batch, e->res_exit_dev,
+                                     (size_t)n * sizeof(sv_exit_result), cudaMemcpyDeviceToHost, e->s_exit)) !=
+                cudaSuccess)
+                return r;
+            if ((r = cudaMemcpyAsync((void*)(e->mb_flag + exit_k), e->meta_dev + e->off_seq, 8,
                                      cudaMemcpyDeviceToHost, e->s_exit)) != cudaSuccess)
                 return r;
-            if ((r = cudaMemcpyAsync((void*)e->mb_flag, e->meta_dev + e->off_seq, 8, cudaMemcpyDeviceToHost,
-                                     e->s_exit)) != cudaSuccess)
-                return r;
-            if ((r = cudaEventRecord(e->ev_join, e->s_exit)) != cudaSuccess) return r;
+            ++exit_k;
+            if (exit_k == n_exits && (r = cudaEventRecord(e->ev_join, e->s_exit)) != cudaSuccess) return r;
         }
     }
-    if ((r = lm_and_accept(st, false)) != cudaSuccess) return r;
+    if ((r = lm_and_accept(st, false, L, 0)) != cudaSuccess) return r;
     if ((r = cudaMemcpyAsync(e->mb_final, e->res_final_dev, (size_t)n * sizeof(sv_exit_result), cudaMemcpyDeviceToHost,
                              st)) != cudaSuccess)
         return r;
-    if (exit_layer > 0)
+    if (n_exits > 0)
         if ((r = cudaStreamWaitEvent(st, e->ev_join, 0)) != cudaSuccess) return r;
 #undef LAUNCH
     *launches = nl;
@@ -869,7 +886,7 @@ static std::map<const FusedPlan*, std::pair<double, double>> g_plan_cost;
 
 // Builds (once per key, outside any stream capture: it allocates and uploads).
 static cudaError_t ensure_plan(sv_engine* e, int n, int gamma, int exit_layer, int nchunk, FusedPlan** out) {
-    StepKey key{n, gamma, exit_layer, nchunk};
+    StepKey key{n, gamma, exit_layer > 0 ? 1ull << (exit_layer - 1) : 0ull, nchunk};
     auto it = e->plans.find(key);
     if (it != e->plans.end()) {
         *out = it->second;
@@ -913,15 +930,16 @@ static cudaError_t issue_fused(sv_engine* e, cudaStream_t st, int n, int gamma, 
     return r;
 }
 
-static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk) {
+static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, uint64_t exit_mask, int nchunk) {
+    const int exit_layer = mask_single_exit(exit_mask);   // fused engine: one exit
     CK(cudaMemcpyAsync(e->meta_dev, e->meta_host, e->meta_bytes, cudaMemcpyHostToDevice, st));
     int nl = 0;
     if (!e->opts.use_graphs || e->prof) {
-        CK(issue_step(e, st, n, gamma, exit_layer, nchunk, &nl));
+        CK(issue_step(e, st, n, gamma, exit_mask, nchunk, &nl));
         e->last_launches = nl;
         return SV_OK;
     }
-    StepKey key{n, gamma, exit_layer, nchunk};
+    StepKey key{n, gamma, exit_mask, nchunk};
     auto it = e->graphs.find(key);
     if (it == e->graphs.end()) {
         if (e->opts.fused) {
@@ -930,7 +948,7 @@ static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, int e
         }
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(e->s_cap, cudaStreamCaptureModeThreadLocal));
-        cudaError_t r = issue_step(e, e->s_cap, n, gamma, exit_layer, nchunk, &nl);
+        cudaError_t r = issue_step(e, e->s_cap, n, gamma, exit_mask, nchunk, &nl);
         cudaError_t r2 = cudaStreamEndCapture(e->s_cap, &g);
         if (r != cudaSuccess) return fail(SV_E_DEVICE, std::string("capture: ") + cudaGetErrorString(r));
         CK(r2);
@@ -944,15 +962,25 @@ static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, int e
     return SV_OK;
 }
 
-extern "C" sv_status sv_verify_submit(sv_engine* e, const sv_verify_req* reqs, int32_t n, int32_t exit_layer,
-                                      sv_exit_result* early, sv_exit_result* final_, void* stream, sv_ticket** out) {
+extern "C" sv_status sv_verify_submit_exits(sv_engine* e, const sv_verify_req* reqs, int32_t n,
+                                            const int32_t* exit_layers, int32_t n_exits, sv_exit_result* early,
+                                            sv_exit_result* final_, void* stream, sv_ticket** out) {
     if (!e || !reqs || !final_ || !out || n < 1) return fail(SV_E_INVALID, "bad arguments");
     std::lock_guard<std::mutex> lk(e->mu);
     if (e->poisoned) return fail(SV_E_DEVICE, "engine poisoned by an earlier CUDA error");
     if (e->inflight) return fail(SV_E_BUSY, "a ticket is already in flight on this engine");
     if (n > e->opts.max_batch) return fail(SV_E_CAPACITY, "n > max_batch");
-    if (exit_layer < 0 || exit_layer > e->L) return fail(SV_E_INVALID, "exit_layer out of range");
-    if (exit_layer > 0 && !early) return fail(SV_E_INVALID, "early result array required when exit_layer > 0");
+    if (n_exits < 0 || n_exits > e->L || (n_exits > 0 && !exit_layers))
+        return fail(SV_E_INVALID, "bad exit layer list");
+    if (n_exits > 0 && !early) return fail(SV_E_INVALID, "early result array required when exits are requested");
+    if (n_exits > 1 && e->opts.fused) return fail(SV_E_INVALID, "the fused engine supports one early exit");
+    if (n_exits > 0 && e->L > 64) return fail(SV_E_INVALID, "early exits need n_layers <= 64");
+    uint64_t exit_mask = 0;
+    for (int k = 0; k < n_exits; ++k) {
+        if (exit_layers[k] < 1 || exit_layers[k] > e->L) return fail(SV_E_INVALID, "exit layer out of range");
+        if (k > 0 && exit_layers[k] <= exit_layers[k - 1]) return fail(SV_E_INVALID, "exit layers must ascend");
+        exit_mask |= 1ull << (exit_layers[k] - 1);
+    }
     const int gamma = reqs[0].gamma;
     if (gamma < 1 || gamma > e->opts.max_gamma) return fail(SV_E_INVALID, "gamma out of range");
     for (int i = 0; i < n; ++i) {
@@ -971,7 +999,9 @@ extern "C" sv_status sv_verify_submit(sv_engine* e, const sv_verify_req* reqs, i
     cudaStream_t st = (cudaStream_t)stream;
     const int G = gamma + 1;
     sv_ticket* t = new sv_ticket();
-    t->e = e; t->n = n; t->early = early; t->final_ = final_; t->exit_layer = exit_layer;
+    t->e = e; t->n = n; t->early = early; t->final_ = final_;
+    t->exits.assign(exit_layers, exit_layers + n_exits);
+    t->exit_done.assign(n_exits, false);
     t->gpu_slot.assign(n, -1);
     t->host_status.assign(n, SV_OK);
     // S0: validate protocol state, build the batch of valid requests
@@ -1036,7 +1066,7 @@ extern "C" sv_status sv_verify_submit(sv_engine* e, const sv_verify_req* reqs, i
     if (t->has_gpu) {
         int nchunk = (max_len + 63) / 64;
         nchunk = std::min(e->max_nchunk, nchunk);   // exact: no empty attention work items
-        sv_status s = run_step(e, st, nb, gamma, exit_layer, nchunk);
+        sv_status s = run_step(e, st, nb, gamma, exit_mask, nchunk);
         if (s) {
             e->poisoned = true;
             for (auto* ss : t->sess) ss->busy = false;
@@ -1050,6 +1080,12 @@ extern "C" sv_status sv_verify_submit(sv_engine* e, const sv_verify_req* reqs, i
     return SV_OK;
 }
 
+extern "C" sv_status sv_verify_submit(sv_engine* e, const sv_verify_req* reqs, int32_t n, int32_t exit_layer,
+                                      sv_exit_result* early, sv_exit_result* final_, void* stream, sv_ticket** out) {
+    if (exit_layer < 0 || (e && exit_layer > e->L)) return fail(SV_E_INVALID, "exit_layer out of range");
+    return sv_verify_submit_exits(e, reqs, n, &exit_layer, exit_layer > 0 ? 1 : 0, early, final_, stream, out);
+}
+
 static void fill_host_result(sv_exit_result* r, const sv_ticket* t, int i, int exit_layer, int is_final) {
     memset(r, 0, sizeof(*r));
     r->round_id = t->rounds[i];
@@ -1060,13 +1096,14 @@ static void fill_host_result(sv_exit_result* r, const sv_ticket* t, int i, int e
     for (int k = 0; k <= SV_MAX_GAMMA; ++k) r->tokens[k] = -1;
 }
 
-extern "C" sv_status sv_wait_early(sv_ticket* t, int64_t timeout_us) {
+extern "C" sv_status sv_wait_exit(sv_ticket* t, int32_t k, int64_t timeout_us) {
     if (!t) return fail(SV_E_INVALID, "NULL ticket");
+    if (k < 0 || k >= (int)t->exits.size()) return fail(SV_E_INVALID, "exit index out of range");
     sv_engine* e = t->e;
-    if (t->exit_layer == 0 || t->early_done) return SV_OK;
+    if (t->exit_done[k]) return SV_OK;
     if (t->has_gpu) {
         const auto t0 = std::chrono::steady_clock::now();
-        while (*e->mb_flag != t->seq) {
+        while (e->mb_flag[k] != t->seq) {
             if (cudaEventQuery(t->ev_done) == cudaSuccess) break;   // step already complete
             if (timeout_us >= 0 &&
                 std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count() >
@@ -1075,11 +1112,32 @@ extern "C" sv_status sv_wait_early(sv_ticket* t, int64_t timeout_us) {
             std::this_thread::yield();
         }
     }
+    const sv_exit_result* row = e->mb_exit + (size_t)k * e->opts.max_batch;
     for (int i = 0; i < t->n; ++i) {
-        if (t->gpu_slot[i] >= 0) t->early[i] = e->mb_exit[t->gpu_slot[i]];
-        else fill_host_result(&t->early[i], t, i, t->exit_layer, 0);
+        sv_exit_result* dst = t->early + (size_t)k * t->n + i;
+        if (t->gpu_slot[i] >= 0) *dst = row[t->gpu_slot[i]];
+        else fill_host_result(dst, t, i, t->exits[k], 0);
     }
-    t->early_done = true;
+    t->exit_done[k] = true;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_exits_ready(sv_ticket* t, int32_t* n_ready) {
+    if (!t || !n_ready) return fail(SV_E_INVALID, "NULL argument");
+    sv_engine* e = t->e;
+    int k = 0;
+    const bool all = !t->has_gpu || cudaEventQuery(t->ev_done) == cudaSuccess;
+    while (k < (int)t->exits.size() && (all || e->mb_flag[k] == t->seq)) ++k;
+    *n_ready = k;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_wait_early(sv_ticket* t, int64_t timeout_us) {
+    if (!t) return fail(SV_E_INVALID, "NULL ticket");
+    for (int k = 0; k < (int)t->exits.size(); ++k) {
+        sv_status s = sv_wait_exit(t, k, timeout_us);
+        if (s) return s;
+    }
     return SV_OK;
 }
 
@@ -1101,7 +1159,7 @@ extern "C" sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us) {
             return fail(SV_E_TIMEOUT, "final result not ready");
         std::this_thread::yield();
     }
-    if (t->exit_layer > 0 && !t->early_done) sv_wait_early(t, -1);
+    sv_wait_early(t, -1);
     std::lock_guard<std::mutex> lk(e->mu);
     for (int i = 0; i < t->n; ++i) {
         sv_session* s = t->sess[i];
@@ -1179,7 +1237,7 @@ extern "C" sv_status sv_debug_logits(sv_ticket* t, int32_t which, float* dst) {
         sv_status s = sv_wait_final(t, -1);
         if (s) return s;
     }
-    if (which == 0 && t->exit_layer == 0) return fail(SV_E_INVALID, "step had no early exit");
+    if (which == 0 && t->exits.empty()) return fail(SV_E_INVALID, "step had no early exit");
     if (!t->has_gpu) return SV_OK;
     const size_t bytes = (size_t)t->nb * (t->gamma + 1) * e->V * 4;
     CK(cudaMemcpy(dst, which == 0 ? e->logits_exit : e->logits_final, bytes, cudaMemcpyDeviceToDevice));

@@ -134,13 +134,13 @@ __global__ void __launch_bounds__(128, 1)
             tma_load_2d(&tmA, sA + i * A_STAGE, &full[i], (kb0 + i) * BK, n0, pol_w);
         }
         pdl_wait();
-        for (int i = 0; i < pre; ++i) tma_load_2d(&tmB, sB + i * C::B_STAGE, &full[i], (kb0 + i) * BK, m0, pol_x);
+        for (int i = 0; i < pre; ++i) tma_load_2d(&tmB, sB + i * C::B_STAGE, &full[i], (kb0 + i) * BK, m0 + a.b_row0, pol_x);
         for (int i = pre; i < nk; ++i) {
             const int s = i % C::STAGES;
             mbar_wait(&empty[s], ((i / C::STAGES) - 1) & 1);
             mbar_arrive_expect_tx(&full[s], C::STAGE);
             tma_load_2d(&tmA, sA + s * A_STAGE, &full[s], (kb0 + i) * BK, n0, pol_w);
-            tma_load_2d(&tmB, sB + s * C::B_STAGE, &full[s], (kb0 + i) * BK, m0, pol_x);
+            tma_load_2d(&tmB, sB + s * C::B_STAGE, &full[s], (kb0 + i) * BK, m0 + a.b_row0, pol_x);
         }
         if (a.pf_map) {   // next GEMM's first K blocks -> L2 (GemmArgs::pf_map)
             const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                         pdl_wait();
                         waited = true;
                     }
-                    tma_load_2d(&tmB, sB + s * C::B_STAGE, &full[s], kb * GB_BK, m0, pol_x);
+                    tma_load_2d(&tmB, sB + s * C::B_STAGE, &full[s], kb * GB_BK, m0 + a.b_row0, pol_x);
                 }
             }
         }

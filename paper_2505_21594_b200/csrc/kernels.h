@@ -31,6 +31,7 @@ struct GemmArgs {
     // problem: out[M, N] = B[M, K] . A[N, K]^T  (A = weights, B = activations)
     int N, K, M, MP;     // MP = padded rows of the activation buffer
     int splits;          // split-K factor (deterministic reduction, fixed order)
+    int b_row0;          // first row of the activation tensor map (exit slot k: k * MP)
     float* ws;           // split-K partials [splits][ntiles][MP][128]
     int* counters;       // [ntiles * mtiles], zero on entry, reset by the reducer
     // RMSNorm folding: rstd[m] = 1/sqrt(sum_t ssq_in[t][m] / d + eps)

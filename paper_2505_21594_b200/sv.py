@@ -97,6 +97,11 @@ EXPORTS = {
     "sv_verify_submit": (C.c_int, [C.c_void_p, C.POINTER(sv_verify_req), C.c_int32, C.c_int32,
                                    C.POINTER(sv_exit_result), C.POINTER(sv_exit_result), C.c_void_p,
                                    C.POINTER(C.c_void_p)]),
+    "sv_verify_submit_exits": (C.c_int, [C.c_void_p, C.POINTER(sv_verify_req), C.c_int32, C.POINTER(C.c_int32),
+                                         C.c_int32, C.POINTER(sv_exit_result), C.POINTER(sv_exit_result),
+                                         C.c_void_p, C.POINTER(C.c_void_p)]),
+    "sv_wait_exit": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
+    "sv_exits_ready": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "sv_wait_early": (C.c_int, [C.c_void_p, C.c_int64]),
     "sv_wait_final": (C.c_int, [C.c_void_p, C.c_int64]),
     "sv_ticket_release": (C.c_int, [C.c_void_p]),
@@ -270,14 +275,26 @@ class Request:
 
 
 class Ticket:
-    def __init__(self, engine, handle, n, early, final, reqs):
+    def __init__(self, engine, handle, n, early, final, reqs, exit_layers=()):
         self.engine, self.h, self.n = engine, handle, n
         self.early, self.final = early, final
+        self.exit_layers = list(exit_layers)
         self._keep = reqs
 
     def wait_early(self, timeout_us: int = -1):
+        """Results of the (first) early exit; all exits are delivered on return."""
         check(lib().sv_wait_early(self.h, timeout_us))
         return [self.early[i] for i in range(self.n)]
+
+    def wait_exit(self, k: int, timeout_us: int = -1):
+        """Results [n] of exit k (the k-th of exit_layers), as soon as it has streamed in."""
+        check(lib().sv_wait_exit(self.h, k, timeout_us))
+        return [self.early[k * self.n + i] for i in range(self.n)]
+
+    def exits_ready(self) -> int:
+        n = C.c_int32()
+        check(lib().sv_exits_ready(self.h, C.byref(n)))
+        return n.value
 
     def wait_final(self, timeout_us: int = -1):
         check(lib().sv_wait_final(self.h, timeout_us))
@@ -333,7 +350,19 @@ class Engine:
         t = C.c_void_p()
         check(lib().sv_verify_submit(self.h, arr, n, exit_layer, early, final, _stream_handle(stream),
                                      C.byref(t)))
-        return Ticket(self, t, n, early, final, (reqs, arr))
+        return Ticket(self, t, n, early, final, (reqs, arr), [exit_layer] if exit_layer else [])
+
+    def submit_exits(self, reqs, exit_layers, stream=None) -> Ticket:
+        """All-exits streaming verify: one early result per layer in exit_layers (ascending)."""
+        n = len(reqs)
+        arr = (sv_verify_req * n)(*[r.to_c() for r in reqs])
+        ex = (C.c_int32 * max(1, len(exit_layers)))(*exit_layers)
+        early = (sv_exit_result * (max(1, len(exit_layers)) * n))()
+        final = (sv_exit_result * n)()
+        t = C.c_void_p()
+        check(lib().sv_verify_submit_exits(self.h, arr, n, ex, len(exit_layers), early, final,
+                                           _stream_handle(stream), C.byref(t)))
+        return Ticket(self, t, n, early, final, (reqs, arr, ex), exit_layers)
 
     def verify(self, reqs, exit_layer: int = 0, stream=None):
         """Submit + wait; returns (early results, final results) lists."""

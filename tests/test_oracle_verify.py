@@ -99,3 +99,24 @@ def test_protocol_errors_leave_session_unchanged():
     assert bad.final.status == acc.E_PROTOCOL and s.cache.length == 12
     ok = verify_step(m, s, 1, 1, [2, 3], None)
     assert ok.final.status == acc.OK and s.cache.length == 12 + 1 + ok.final.accepted
+
+
+def test_all_exits_match_single_exit_runs():
+    """All-exits verify (Alg-S): the exit list gives, for every
+    layer, exactly the single-exit result of that layer (same counters, read-only),
+    the final result is unchanged by the exits, and the exit at l = L equals it."""
+    cfg = tiny().__class__(**{**tiny().__dict__, "n_layers": 4})
+    m = om.Model(cfg, 1)
+    x, q = timing_drafts(5, 1, 4, cfg.vocab)
+    ref = verify_step(m, _session(cfg, m, prefill=False), 1, 7, x[0], q[0])
+    out = verify_step(m, _session(cfg, m, prefill=False), 1, 7, x[0], q[0], exit_layers=[1, 2, 3, 4])
+    assert [le for le, _, _ in out.exits] == [1, 2, 3, 4]
+    assert out.final.tokens == ref.final.tokens and np.array_equal(out.final_logits, ref.final_logits)
+    assert out.new_len == ref.new_len
+    for le, r, z in out.exits:
+        single = verify_step(m, _session(cfg, m, prefill=False), 1, 7, x[0], q[0], exit_layer=le)
+        assert np.array_equal(z, single.exit_logits)
+        assert r.tokens == single.early.tokens and r.accepted == single.early.accepted
+        assert r.score == single.early.score
+    le, r, z = out.exits[-1]
+    assert np.array_equal(z, out.final_logits) and r.tokens == out.final.tokens
