@@ -255,6 +255,14 @@ class OracleSample:
                 f"{t32:.2f} s; weight generation excluded")
 
 
+def expected_tau(gamma, alpha):
+    """Tokens per verify step of the calibrated workload: every drafted position is
+    accepted with probability alpha (the drafts are calibrated to sum_v min(p, q) =
+    alpha), so E[delta + 1] = sum_{k=0..gamma} alpha^k (alpha_j = alpha).
+    A property of the workload definition, used for the CPU arms' tokens/s."""
+    return float(sum(alpha ** k for k in range(gamma + 1)))
+
+
 def host_cores():
     try:
         from threadpoolctl import threadpool_info
@@ -276,7 +284,7 @@ def run_reference(args):
             times.append(t32)
             toks.append(tps)
     sec = float(np.mean(times))
-    tok = float(np.mean(toks))
+    tok = expected_tau(args.gamma, args.alpha)
     value = per * tok / sec
     cores, desc = host_cores(), sample.describe(sec)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -285,8 +293,8 @@ def run_reference(args):
             "config": {"workload": f"{args.config} Llama2-7B shape, B={per}, ctx {ctx}, gamma {args.gamma}",
                        "global_batch": per, "seq_len": ctx, "parallelism": "host cores"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": desc + f"; tokens/step {tok:.3f} from the oracle's own decisions "
-                                       "(timing-mode Zipf drafts)"},
+                             "sample": desc + f"; tokens/step {tok:.3f} = expected tau of the calibrated "
+                                       f"workload (alpha {args.alpha}, gamma {args.gamma})"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -315,7 +323,7 @@ def run_ours(args):
         exit_layer = 0
     W = sv.Weights(mc, seed=1, device=local)
     blocks_per = (ctx + gamma + 1 + 63) // 64
-    eng = sv.Engine(mc, W, max_batch=per, max_gamma=gamma, kv_blocks=per * blocks_per, device=local)
+    eng = sv.Engine(mc, W, max_batch=per, max_gamma=max(1, gamma), kv_blocks=per * blocks_per, device=local)
     sessions = []
     for rid in shard(total, world, rank):          # contiguous shard of the request ids
         s = eng.open_session(rid + 1, 0x5EED0000 + rid)
@@ -328,8 +336,13 @@ def run_ours(args):
     sets = [build_calibrated_drafts(sv, eng, sessions, pend, ctx, gamma, args.alpha, mc.vocab,
                                     7 + 1000 * rank + k, rounds) for k in range(n_sets)]
     xs = [x for x, _ in sets]
-    q_dev = [torch.from_numpy(q).cuda() for _, q in sets]
-    q_host = [torch.from_numpy(q).pin_memory().numpy() for _, q in sets]
+    if gamma == 0:   # plain AR step ("Cloud AR"): sample p_0, probs pointer never read
+        dummy = torch.empty(per, 1, device="cuda")
+        q_dev = [dummy for _ in sets]
+        q_host = [np.zeros((per, 1), dtype=np.float32) for _ in sets]
+    else:
+        q_dev = [torch.from_numpy(q).cuda() for _, q in sets]
+        q_host = [torch.from_numpy(q).pin_memory().numpy() for _, q in sets]
     stream = torch.cuda.current_stream()
     counter = [0]
 
@@ -453,11 +466,12 @@ def run_ours(args):
         sample = OracleSample(args, ctx)
         t32, _ = sample.step()
         cores, desc = host_cores(), sample.describe(t32)
-        tps = tokens / args.steps
+        tps = expected_tau(gamma, args.alpha)
         cpu = {"value": tps / t32, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": desc + f"; tokens/step {tps:.3f} taken from this workload's verified decisions"}
+               "sample": desc + f"; tokens/step {tps:.3f} = expected tau of the calibrated workload "
+                                f"(alpha {args.alpha}, gamma {gamma})"}
 
-    h2d = per * gamma * mc.vocab * 4 + per * (gamma + 1) * 12
+    h2d = per * gamma * mc.vocab * 4 + per * (gamma + 1) * 12   # gamma 0: no draft probabilities
     d2h = 2 * per * 64
     line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max * 1e3 / args.steps, 4),

@@ -153,8 +153,12 @@ typedef struct {
     int32_t prefix_len;           /* tokens the client holds incl. pending
                                      (= cached_len + 1), else SV_E_PROTOCOL        */
     int32_t pending_token;        /* last verified token; its KV is written here   */
-    int32_t gamma;                /* 1..max_gamma, equal for all requests of a submit */
-    const int32_t* draft_tokens;  /* host [gamma]: x_1..x_gamma                     */
+    int32_t gamma;                /* 0..max_gamma, equal for all requests of a submit;
+                                     0 = plain autoregressive step (SURVEY.md §8(f) NEXT-2,
+                                     "Cloud AR"): one query row, next token
+                                     = argmax p_0 (draft_probs NULL) or a sample of p_0
+                                     (draft_probs any non-NULL pointer, never read)      */
+    const int32_t* draft_tokens;  /* host [gamma]: x_1..x_gamma (may be NULL if gamma = 0) */
     const float* draft_probs;     /* [gamma][vocab] fp32, row j-1 = q_j; NULL => greedy */
     int32_t probs_on_host;        /* 0: draft_probs is a device pointer, 1: host    */
 } sv_verify_req;

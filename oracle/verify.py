@@ -46,8 +46,8 @@ def verify_step(model: Model, sess: Session, round_id: int, pending: int, drafts
     cfg = model.cfg
     drafts = [int(x) for x in drafts]
     gamma = len(drafts)
-    if not (1 <= gamma <= 8):
-        raise ValueError("gamma must be in 1..8")
+    if not (0 <= gamma <= 8):          # gamma = 0: the plain autoregressive step ("Cloud AR",
+        raise ValueError("gamma must be in 0..8")   # PAPER.md:318): one query, next token from p_0
     if round_id != sess.last_round + 1:
         bad = acc.Result(0, [], 0.0, 0.0, acc.E_PROTOCOL, [])
         return StepOut(bad, bad, None, None, sess.cache.length)

@@ -974,6 +974,7 @@ extern "C" sv_status sv_verify_submit_exits(sv_engine* e, const sv_verify_req* r
         return fail(SV_E_INVALID, "bad exit layer list");
     if (n_exits > 0 && !early) return fail(SV_E_INVALID, "early result array required when exits are requested");
     if (n_exits > 1 && e->opts.fused) return fail(SV_E_INVALID, "the fused engine supports one early exit");
+    if (reqs[0].gamma == 0 && e->opts.fused) return fail(SV_E_INVALID, "the fused engine needs gamma >= 1");
     if (n_exits > 0 && e->L > 64) return fail(SV_E_INVALID, "early exits need n_layers <= 64");
     uint64_t exit_mask = 0;
     for (int k = 0; k < n_exits; ++k) {
@@ -982,12 +983,12 @@ extern "C" sv_status sv_verify_submit_exits(sv_engine* e, const sv_verify_req* r
         exit_mask |= 1ull << (exit_layers[k] - 1);
     }
     const int gamma = reqs[0].gamma;
-    if (gamma < 1 || gamma > e->opts.max_gamma) return fail(SV_E_INVALID, "gamma out of range");
+    if (gamma < 0 || gamma > e->opts.max_gamma) return fail(SV_E_INVALID, "gamma out of range");
     for (int i = 0; i < n; ++i) {
         const sv_verify_req& q = reqs[i];
         if (!q.session || q.session->e != e) return fail(SV_E_INVALID, "request without a session of this engine");
         if (q.gamma != gamma) return fail(SV_E_INVALID, "gamma must be equal for all requests of a submit");
-        if (!q.draft_tokens) return fail(SV_E_INVALID, "draft_tokens is NULL");
+        if (!q.draft_tokens && gamma > 0) return fail(SV_E_INVALID, "draft_tokens is NULL");
         if (q.pending_token < 0 || q.pending_token >= e->V) return fail(SV_E_INVALID, "pending token out of range");
         for (int j = 0; j < gamma; ++j)
             if (q.draft_tokens[j] < 0 || q.draft_tokens[j] >= e->V) return fail(SV_E_INVALID, "draft token out of range");
@@ -1250,7 +1251,7 @@ extern "C" sv_status sv_debug_accept(sv_engine* e, const float* logits_dev, cons
     std::lock_guard<std::mutex> lk(e->mu);
     if (e->inflight) return fail(SV_E_BUSY, "a ticket is in flight");
     const int gamma = reqs[0].gamma;
-    if (gamma < 1 || gamma > e->opts.max_gamma) return fail(SV_E_INVALID, "gamma out of range");
+    if (gamma < 0 || gamma > e->opts.max_gamma) return fail(SV_E_INVALID, "gamma out of range");
     CK(cudaSetDevice(e->device));
     ReqDev* rd = (ReqDev*)(e->meta_host + e->off_reqdev);
     for (int i = 0; i < n; ++i) {

@@ -182,3 +182,20 @@ def test_margins_recorded():
     r = acc.accept_greedy(z, [1, 2])
     assert [k for k, _, _ in r.margins] == ["argmax", "argmax", "argmax"]
     assert r.min_margin == pytest.approx(0.5)
+
+
+def test_gamma_zero_ar_step():
+    """gamma = 0 (plain AR step): no drafts, delta = 0; greedy emits
+    argmax z_0, sampling emits a draw from p_0 = softmax(z_0) (chi-square)."""
+    rng = np.random.default_rng(8)
+    V, N = 7, 20000
+    p0 = _rows(rng, 1, V, conc=1.5)
+    z = np.log(p0)
+    g = acc.accept(z, [])
+    assert g.accepted == 0 and g.tokens == [int(np.argmax(z[0]))]
+    counts = np.zeros(V)
+    for t in range(N):
+        r = acc.accept(z, [], np.zeros((0, V)), seed=3, session_id=2, round_id=t + 1)
+        assert r.accepted == 0 and len(r.tokens) == 1
+        counts[r.tokens[0]] += 1
+    assert stats.chisquare(counts, N * p0[0]).pvalue > 1e-3

@@ -1,0 +1,22 @@
+# Round-end measurement set: bench lines (C2 default with the CPU oracle baseline,
+# C3 sweeps, C4, C5, all-exits), ncu launch list + full capture summary.
+export PYTHONUNBUFFERED=1
+OUT=gpurun_out/final
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/gpu.txt
+timeout 900 python bench.py > $OUT/c2.json 2> $OUT/c2.err
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/reference.json 2> $OUT/reference.err
+for g in 1 2 3 4 5 6 7 8; do timeout 300 python bench.py --config C3 --gamma $g --steps 20 --warmup 3 --no-cpu-baseline > $OUT/c3_g$g.json 2>/dev/null; done
+for e in 8 24; do timeout 300 python bench.py --config C3 --exit-layer $e --steps 20 --warmup 3 --no-cpu-baseline > $OUT/c3_e$e.json 2>/dev/null; done
+timeout 300 python bench.py --all-exits --steps 20 --warmup 3 --no-cpu-baseline > $OUT/c2_all_exits.json 2>/dev/null
+timeout 600 python bench.py --config C5 --steps 10 --warmup 3 --no-cpu-baseline > $OUT/c5.json 2>/dev/null
+timeout 900 python bench.py --config C4 --steps 5 --warmup 3 --no-cpu-baseline > $OUT/c4.json 2>/dev/null
+ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/c2_launches.csv python tools/ncu_step.py > $OUT/ncu_list.log 2>&1
+ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"gemm_kernel|attn3" -c 10 -o $OUT/c2_full python tools/ncu_step.py > $OUT/ncu_full.log 2>&1
+python tools/ncu_summarize.py --list $OUT/c2_launches.csv --full $OUT/c2_full.ncu-rep --out $OUT/ncu_summary.json --source "C2 (Llama2-7B shape, B=1, ctx 512, gamma 4, exit 16): ncu launch list of one step (cold-cache, serialised) + --set full on the first 10 gemm/attention launches" > /dev/null
+for f in $OUT/*.json; do python -c "
+import json,sys
+d=json.load(open('$f'))
+if 'roofline' in d: print('$f', d.get('latency_p50_ms'), d['value'], d['roofline']['frac'], d['roofline']['step_frac_of_peak'])
+elif 'impl' in d: print('$f', d.get('value'), d.get('ms_per_step'))
+" 2>/dev/null; done
