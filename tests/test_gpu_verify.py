@@ -271,3 +271,43 @@ def test_7b_width_two_layers(svlib, fused):
     print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
     assert errs.max() < LOGIT_TOL
     assert not tf.hard_mismatch and not te.hard_mismatch
+
+
+def test_7b_width_c5_batch(svlib):
+    """configs[4]-shaped batch at the Llama2-7B layer shapes (2 layers): B = 16
+    requests x (gamma + 1) = 80 query rows -> the persistent 128-token GEMM and the
+    2-stage attention ring, in bench.py's launch configuration; sampled
+    requests {0, 7, 15} against the fp64 oracle, one stochastic round."""
+    from paper_2505_21594_b200 import sv
+    mc = ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=640)
+    B, gamma, ctx = 16, 4, 600
+    W = sv.Weights(mc, seed=1)
+    eng = sv.Engine(mc, W, max_batch=B, max_gamma=gamma)
+    model = om.Model(mc, seed=1)
+    ss = []
+    for b in range(B):
+        s = eng.open_session(60 + b, 70 + b)
+        s.fill_kv(ctx, kv_seed=80 + b)
+        ss.append(s)
+    x, q = wd.timing_drafts(33, B, gamma, mc.vocab, s=1.1)
+    qd = torch.from_numpy(q).cuda()
+    t = eng.submit([sv.Request(ss[b], 1, 5 + b, x[b], qd[b]) for b in range(B)], exit_layer=1)
+    early = t.wait_early()
+    final = t.wait_final()
+    zf = t.logits(1, gamma).cpu().numpy()
+    ze = t.logits(0, gamma).cpu().numpy()
+    t.release()
+    tally = Tally()
+    for b in (0, 7, 15):
+        osess = oracle_session(mc, model, 60 + b, 70 + b, 80 + b, ctx)
+        out = verify_step(model, osess, 1, 5 + b, x[b], q[b].astype(np.float64), exit_layer=1)
+        rel, eps = row_rel_err(zf[b], out.final_logits)
+        rel_e, eps_e = row_rel_err(ze[b], out.exit_logits)
+        assert rel.max() < LOGIT_TOL and rel_e.max() < LOGIT_TOL
+        tally.add(out.final, final[b], decision_bound(eps.max()), tag=("final", b))
+        tally.add(out.early, early[b], decision_bound(eps_e.max()), tag=("exit", b))
+    print(tally.report())
+    assert not tally.hard_mismatch
+    for s in ss:
+        s.close()
+    eng.close()
