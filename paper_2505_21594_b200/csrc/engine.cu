@@ -182,6 +182,7 @@ struct sv_engine {
     sv_engine_opts opts;
     int device, num_sms;
     int pf_depth = 0;                           // GemmArgs::pf_depth (env SV_PF)
+    bool no_box = false;                        // env SV_NO_BOX: load full token tiles
     int attn_splits = 0;                        // attention split override (env SV_ATTN_SPLITS; 0 = attn3_splits)
     std::vector<CUtensorMap> wmap128;           // weight maps [qkv L][o L][gu L][down L][lm] (box rows 128)
     // weights
@@ -221,6 +222,7 @@ struct sv_engine {
     std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;
     CUtensorMap tm_lm;
     std::map<int, std::vector<CUtensorMap>> tm_act;   // tile_n -> {u, attn_out, act, u_exit}
+    std::map<int, std::vector<CUtensorMap>> tm_box;   // box rows -> {u, attn_out, act, u_exit} (M < tile_n)
     // streams / graphs
     cudaStream_t s_cap, s_exit;
     cudaEvent_t ev_fork, ev_join;
@@ -396,6 +398,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (const char* as = getenv("SV_ATTN_SPLITS")) e->attn_splits = atoi(as);
     if (getenv("SV_ATTN_RING2")) g_attn_ring1 = false;
     if (getenv("SV_SPLIT_ANY")) g_split_any = true;
+    if (getenv("SV_NO_BOX")) e->no_box = true;
     e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
     e->L = cfg->n_layers; e->d = cfg->d_model; e->F = cfg->d_ff; e->V = cfg->vocab;
     e->H = cfg->n_heads; e->D = cfg->head_dim;
@@ -621,8 +624,23 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         a.ktrace = e->ktrace;
         a.ktrace_id = nl;
         const CUtensorMap& A = e->wmap128[wid];
-        const CUtensorMap& B = tma[bbuf];
         a.splits = gemm_pick_splits(N, K, M, tn, e->num_sms);
+        const CUtensorMap* Bp = &tma[bbuf];
+        if (M < tn && !e->no_box) {   // one token tile: load only its real rows
+            const int box = (M + 7) / 8 * 8;
+            auto it = e->tm_box.find(box);
+            if (it == e->tm_box.end()) {
+                std::vector<CUtensorMap> m(4);
+                if (!make_tmap_bf16(&m[0], e->u, e->MP, d, box) || !make_tmap_bf16(&m[1], e->attn_out, e->MP, d, box) ||
+                    !make_tmap_bf16(&m[2], e->act, e->MP, F, box) ||
+                    !make_tmap_bf16(&m[3], e->u_exit, (uint64_t)e->L * e->MP, d, box))
+                    return cudaErrorInvalidValue;
+                it = e->tm_box.emplace(box, m).first;
+            }
+            Bp = &it->second[bbuf];
+            a.b_box = box;
+        }
+        const CUtensorMap& B = *Bp;
         if (nx >= 0 && tn <= 64 && e->pf_depth > 0) {
             a.pf_map = e->d_tmaps + nx;
             a.pf_tiles = nN / 128;

@@ -128,9 +128,12 @@ __global__ void __launch_bounds__(128, 1)
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer
         const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+        // the activation box holds only the tile's real token rows (GemmArgs::b_box);
+        // the MMA's other B rows read stale smem into output columns never stored
+        const uint32_t stage_tx = A_STAGE + (a.b_box ? a.b_box : TN) * BK * 2;
         const int pre = nk < C::STAGES ? nk : C::STAGES;
         for (int i = 0; i < pre; ++i) {   // weights do not depend on the previous kernel
-            mbar_arrive_expect_tx(&full[i], C::STAGE);
+            mbar_arrive_expect_tx(&full[i], stage_tx);
             tma_load_2d(&tmA, sA + i * A_STAGE, &full[i], (kb0 + i) * BK, n0, pol_w);
         }
         pdl_wait();
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(128, 1)
         for (int i = pre; i < nk; ++i) {
             const int s = i % C::STAGES;
             mbar_wait(&empty[s], ((i / C::STAGES) - 1) & 1);
-            mbar_arrive_expect_tx(&full[s], C::STAGE);
+            mbar_arrive_expect_tx(&full[s], stage_tx);
             tma_load_2d(&tmA, sA + s * A_STAGE, &full[s], (kb0 + i) * BK, n0, pol_w);
             tma_load_2d(&tmB, sB + s * C::B_STAGE, &full[s], (kb0 + i) * BK, m0 + a.b_row0, pol_x);
         }

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
     if (warp == 8) {
         if (lane == 0) {   // ------------------------------------------ producer
             const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+            const uint32_t stage_tx = GB_A + (a.b_box ? a.b_box : TN) * GB_BK * 2;   // GemmArgs::b_box
             int it = 0;
             bool waited = false;
             for (int t = blockIdx.x; t < T; t += gridDim.x) {
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                 for (int kb = 0; kb < KB; ++kb, ++it) {
                     const int s = it % C::STAGES;
                     if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
-                    mbar_arrive_expect_tx(&full[s], C::STAGE);
+                    mbar_arrive_expect_tx(&full[s], stage_tx);
                     tma_load_2d(&tmA, sA + s * GB_A, &full[s], kb * GB_BK, n0, pol_w);
                     if (!waited) {     // weights above never depend on the previous kernel
                         pdl_wait();

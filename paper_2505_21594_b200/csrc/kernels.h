@@ -32,6 +32,7 @@ struct GemmArgs {
     int N, K, M, MP;     // MP = padded rows of the activation buffer
     int splits;          // split-K factor (deterministic reduction, fixed order)
     int b_row0;          // first row of the activation tensor map (exit slot k: k * MP)
+    int b_box;           // rows of the activation TMA box (<= tile_n; 0 = tile_n), M <= tile_n only
     float* ws;           // split-K partials [splits][ntiles][MP][128]
     int* counters;       // [ntiles * mtiles], zero on entry, reset by the reducer
     // RMSNorm folding: rstd[m] = 1/sqrt(sum_t ssq_in[t][m] / d + eps)
