@@ -41,7 +41,7 @@ extern "C" {
 #endif
 
 #define SV_MAX_GAMMA 8
-#define SV_ABI_VERSION 1
+#define SV_ABI_VERSION 2
 
 typedef enum {
     SV_OK = 0,
@@ -121,6 +121,9 @@ typedef struct {
     int32_t fused;       /* 1: the whole step is ONE persistent kernel (one CTA per
                             SM, stream-K GEMM segments, device-side dependency
                             counters); 0: one kernel per op       */
+    int32_t max_prefill; /* max prompt tokens of one sv_prefill (0 = no prefill;
+                            sizes the activation buffers: rows = max(max_batch *
+                            (max_gamma + 1), max_prefill))                      */
 } sv_engine_opts;
 
 /* kv_pool: device memory (caller-owned, >= one KV block), carved into blocks of
@@ -210,6 +213,15 @@ SV_API sv_status sv_wait_exit(sv_ticket* t, int32_t k, int64_t timeout_us);
  * results have reached host memory. */
 SV_API sv_status sv_exits_ready(sv_ticket* t, int32_t* n_ready);
 SV_API sv_status sv_ticket_release(sv_ticket* t);
+
+/* Prefill: append the prompt tokens[0..n) to the
+ * session's KV cache in one pass (positions len..len+n-1, causal inside the
+ * prompt, Eq. 3) and emit the next token from the last prompt row:
+ * argmax (sample = 0) or a sample of p (sample = 1; the session's Philox stream at
+ * round_id = last_round + 1, which the call consumes).  out->tokens[0] = next
+ * token (the pending token of the first verify round), out->new_len = len + n.
+ * Synchronous; n <= opts.max_prefill (SV_E_CAPACITY), per-op engine only. */
+SV_API sv_status sv_prefill(sv_session* s, const int32_t* tokens, int32_t n, int32_t sample, sv_exit_result* out);
 
 /* The north star's synchronous form: verify(draft_tokens, draft_probs, kv) ->
  * accepted_len, early_exit_token, next_token, for one request. */

@@ -69,3 +69,20 @@ def verify_step(model: Model, sess: Session, round_id: int, pending: int, drafts
     sess.cache.truncate(new_len)                      # S14 rollback
     sess.last_round = round_id
     return StepOut(final, early, z, ze, new_len, exits)
+
+
+def prefill_step(model: Model, sess: Session, round_id: int, tokens, sample: bool = False):
+    """Prefill: run the prompt block through all layers
+    (Eq. 3, causal inside the block), keep all its K/V rows, and
+    emit the next token from the last row: argmax, or a race sample of p with the
+    session's counters at round_id (the gamma = 0 acceptance, R2).
+    Returns (Result, last-row logits [1, V])."""
+    if round_id != sess.last_round + 1:
+        raise ValueError("round_id must be last_round + 1")
+    tokens = np.asarray(tokens, dtype=np.int64)
+    z, _, _ = forward(model, sess.cache, tokens)        # cache.length += len(tokens)
+    zl = z[-1:]
+    q = np.zeros((0, zl.shape[1])) if sample else None
+    res = acc.accept(zl, [], q, seed=sess.philox_seed, session_id=sess.session_id, round_id=round_id)
+    sess.last_round = round_id
+    return res, zl

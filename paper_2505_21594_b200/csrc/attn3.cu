@@ -117,7 +117,9 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     // griddepcontrol.wait and overlap the QKV GEMM; q and the gamma+1 new rows
     // (this step's QKV epilogue) are only touched after it.
     const int ctx = a.ctx[b];
-    const int T = ctx + G;
+    const int Gb = a.g_rows ? a.g_rows[b] : G;          // valid query rows of this request
+    const int cpre = a.ctx_pre ? a.ctx_pre[b] : ctx;    // rows written before this step
+    const int T = ctx + Gb;
     const int npg = (T + 63) / 64;
     const int p0 = (int)((long long)npg * r / S), p1 = (int)((long long)npg * (r + 1) / S);
     const int np = p1 - p0;
@@ -148,7 +150,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     // chunk ci holds only cached rows iff its last key < ctx; such chunks form a
     // prefix of this warp's sequence, so commit order stays the chunk order
     int pre = 0;
-    while (pre < NST && pre < n_my && (p0 * 64 + (warp + A3_WARPS * pre + 1) * A3_CHUNK) <= ctx) {
+    while (pre < NST && pre < n_my && (p0 * 64 + (warp + A3_WARPS * pre + 1) * A3_CHUNK) <= cpre) {
         issue(warp + A3_WARPS * pre, pre);
         ++pre;
     }
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             float lo = 0.f, hi = 0.f;
-            if (row < G) {
+            if (row < Gb) {
                 const float* qp = a.q + (size_t)(b * G + row) * a.d_model + h * A3_D + c * 8 + 2 * u;
                 lo = qp[0] * a.scale_log2;
                 hi = qp[1] * a.scale_log2;
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
             for (int e = 0; e < 4; ++e) {
                 const int j = (e < 2) ? row0 : row1;
                 const int kabs = kabs0 + 8 * n + 2 * t4 + (e & 1);
-                if (j >= G || kabs > ctx + j) sacc[n][e] = -INFINITY;
+                if (j >= Gb || kabs > ctx + j) sacc[n][e] = -INFINITY;
                 mnew[e >> 1] = fmaxf(mnew[e >> 1], sacc[n][e]);
             }
 #pragma unroll
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     }
     __syncthreads();
     A3_STAMP(5);
-    for (int i = tid; i < G * A3_D; i += 128) {
+    for (int i = tid; i < Gb * A3_D; i += 128) {
         const int j = i / A3_D, d = i % A3_D;
         float O = 0.f;
         for (int w = 0; w < A3_WARPS; ++w) O = fmaf(mO[(w * 16 + j) * A3_D + d], mM[w * 16 + j], O);
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     A3_STAMP(6);
     {   // every rank merges a slice of the G x 128 outputs (rank order of the sum: deterministic)
         const int rk = (int)cluster_rank3();
-        for (int i = rk * 128 + tid; i < G * A3_D; i += S * 128) {
+        for (int i = rk * 128 + tid; i < Gb * A3_D; i += S * 128) {
             const int j = i / A3_D, d = i % A3_D;
             float mq[8], lq[8], oq[8];
 #pragma unroll

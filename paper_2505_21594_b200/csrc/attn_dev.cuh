@@ -39,7 +39,8 @@ __device__ bool attn_page_body(const AttnArgs& a, int bh, int c, int tid, AttnSm
     const int G = a.G;
     const int ctx = a.ctx[b];                          // both loads issued together
     const int blk = a.page_table[b * a.pt_stride + c];  // (in bounds; unused if c is past the end)
-    const int T = ctx + G;
+    const int Gb = a.g_rows ? a.g_rows[b] : G;         // valid query rows (prefill blocks)
+    const int T = ctx + Gb;
     const int nch_b = (T + KPAGE - 1) / KPAGE;
     if (c >= nch_b) return false;
     const int k0 = c * KPAGE;

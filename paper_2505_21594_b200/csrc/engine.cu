@@ -196,6 +196,11 @@ struct sv_engine {
     int pt_stride;
     // sizes
     int max_rows, MP, d, F, V, L, H, D;
+    int max_vreq = 1;                           // meta capacity: requests or prefill query blocks
+    struct {                                    // set by sv_prefill for the duration of one issue_step
+        bool on = false;
+        int n_tokens = 0, nq = 0, gb = 0;
+    } pf;
     // device scratch
     float *h, *qbuf, *ssq, *logits_exit, *logits_final, *ws_main, *ws_exit, *rope, *attn_o, *attn_ml;
     bf16_raw_t *u, *u_exit, *attn_out, *act;
@@ -208,7 +213,7 @@ struct sv_engine {
     float* probs_stage = nullptr;               // device copy of host draft probs
     // per-step metadata (device + pinned staging, same layout)
     uint8_t *meta_dev, *meta_host;
-    size_t meta_bytes, off_tok, off_pos, off_req, off_ctx, off_pt, off_reqdev, off_seq;
+    size_t meta_bytes, off_tok, off_pos, off_req, off_ctx, off_pt, off_reqdev, off_seq, off_grows, off_cpre;
     // pinned mailboxes
     sv_exit_result *mb_exit, *mb_final;
     volatile uint64_t* mb_flag;
@@ -275,8 +280,9 @@ static sv_status engine_alloc(sv_engine* e) {
     CK(dalloc((void**)&e->cnt_exit, (size_t)max_tiles * 4));
     // attention partials
     e->max_nchunk = e->cfg.max_ctx / 64 + 1;
-    const size_t bh = (size_t)e->opts.max_batch * e->H;
-    const int G = e->opts.max_gamma + 1;
+    // per-page attention partials (attn_kernel, head_dim != 128, and the fused kernel)
+    const size_t bh = (size_t)(e->D == 128 ? e->opts.max_batch : e->max_vreq) * e->H;
+    const int G = std::max(e->opts.max_gamma + 1, 8);
     CK(dalloc((void**)&e->attn_o, bh * e->max_nchunk * G * e->D * 4));
     CK(dalloc((void**)&e->attn_ml, bh * e->max_nchunk * G * 2 * 4));
     CK(dalloc((void**)&e->cnt_attn, bh * 4));
@@ -304,13 +310,15 @@ static sv_status engine_alloc(sv_engine* e) {
         CK(cudaMemcpy(e->rope, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
     }
     // metadata block
-    const int B = e->opts.max_batch;
+    const int B = e->opts.max_batch, VB = e->max_vreq;
     size_t off = 0;
     e->off_tok = off; off = align_up(off + (size_t)MP * 4, 256);
     e->off_pos = off; off = align_up(off + (size_t)MP * 4, 256);
     e->off_req = off; off = align_up(off + (size_t)MP * 4, 256);
-    e->off_ctx = off; off = align_up(off + (size_t)B * 4, 256);
-    e->off_pt = off; off = align_up(off + (size_t)B * e->pt_stride * 4, 256);
+    e->off_ctx = off; off = align_up(off + (size_t)VB * 4, 256);
+    e->off_pt = off; off = align_up(off + (size_t)VB * e->pt_stride * 4, 256);
+    e->off_grows = off; off = align_up(off + (size_t)VB * 4, 256);
+    e->off_cpre = off; off = align_up(off + (size_t)VB * 4, 256);
     e->off_reqdev = off; off = align_up(off + (size_t)B * sizeof(ReqDev), 256);
     e->off_seq = off; off = align_up(off + 8, 256);
     e->meta_bytes = off;
@@ -385,7 +393,8 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     sv_status s = check_cfg(cfg);
     if (s) return s;
     if (!w || !opts || !out || !kv_pool) return fail(SV_E_INVALID, "NULL argument");
-    if (opts->max_batch < 1 || opts->max_gamma < 1 || opts->max_gamma > SV_MAX_GAMMA)
+    if (opts->max_batch < 1 || opts->max_gamma < 1 || opts->max_gamma > SV_MAX_GAMMA || opts->max_prefill < 0 ||
+        opts->max_prefill > cfg->max_ctx)
         return fail(SV_E_INVALID, "bad engine options");
     if ((s = require_sm100(device))) return s;
     CK(cudaSetDevice(device));
@@ -412,7 +421,8 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (e->nblocks < 1) { delete e; return fail(SV_E_CAPACITY, "kv pool smaller than one block"); }
     for (int i = e->nblocks - 1; i >= 0; --i) e->free_blocks.push_back(i);
     e->pt_stride = cfg->max_ctx / cfg->page_tokens + 1;
-    e->max_rows = opts->max_batch * (opts->max_gamma + 1);
+    e->max_rows = std::max(opts->max_batch * (opts->max_gamma + 1), opts->max_prefill);
+    e->max_vreq = std::max(opts->max_batch, (opts->max_prefill + 7) / 8);
     e->MP = (int)align_up((size_t)e->max_rows, 256);
     if ((s = engine_alloc(e)) || (s = engine_tmaps(e))) {
         delete e;
@@ -558,7 +568,9 @@ static int mask_single_exit(uint64_t mask) {   // the exit layer of a one-exit m
 static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, uint64_t exit_mask, int nchunk,
                               int* launches) {
     if (e->opts.fused) return issue_fused(e, st, n, gamma, mask_single_exit(exit_mask), nchunk, launches);
-    const int G = gamma + 1, M = n * G, d = e->d, F = e->F, V = e->V, L = e->L;
+    const bool pf = e->pf.on;                 // prefill: one session's prompt as query blocks
+    const int G = gamma + 1, M = pf ? e->pf.n_tokens : n * G, d = e->d, F = e->F, V = e->V, L = e->L;
+    const int nA = pf ? e->pf.nq : n, GA = pf ? e->pf.gb : G;   // attention "requests" and their rows
     const int tn = gemm_pick_tile_n(M);
     const auto& tma = e->tm_act[tn];   // {u, attn_out, act, u_exit}
     int nl = 0;
@@ -605,10 +617,10 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
     int max_ctx = 0;
     {
         const int32_t* ctxh = (const int32_t*)(e->meta_host + e->off_ctx);
-        for (int b = 0; b < n; ++b) {
+        for (int b = 0; b < nA; ++b) {
             max_ctx = std::max(max_ctx, (int)ctxh[b]);
-            attn_bytes += (double)(ctxh[b] + G) * d * 4;
-            for (int j = 0; j < G; ++j) attn_flops += 4.0 * (ctxh[b] + j + 1) * d;
+            attn_bytes += (double)(ctxh[b] + GA) * d * 4;
+            for (int j = 0; j < GA; ++j) attn_flops += 4.0 * (ctxh[b] + j + 1) * d;
         }
     }
 
@@ -651,9 +663,13 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         return gemm_launch(epi, tn, A, B, a, s);
     };
     auto lm_and_accept = [&](cudaStream_t s, bool is_exit, int exit_layer, int slot) -> cudaError_t {
-        GemmArgs a = base_args(e, M);
+        GemmArgs a = base_args(e, pf ? 1 : M);
         a.ssq_in = ssq_at(e, is_exit ? exit_layer : L, 0);
         a.b_row0 = is_exit ? slot * e->MP : 0;
+        if (pf) {   // prefill: the LM head of the last prompt row only (its next token)
+            a.b_row0 = e->pf.n_tokens - 1;
+            a.ssq_in += e->pf.n_tokens - 1;
+        }
         a.logits = is_exit ? e->logits_exit : e->logits_final;
         cudaError_t q;
         LAUNCH(is_exit ? SV_K_LM_EXIT : SV_K_LM_FINAL, -1, s, gemm_bytes(V, d, (double)M * V * 4),
@@ -665,7 +681,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         aa.race = is_exit ? e->race_exit : e->race_final;
         aa.counters = is_exit ? e->cnt_acc_exit : e->cnt_acc_final;
         aa.out = is_exit ? e->res_exit_dev : e->res_final_dev;
-        aa.B = n; aa.G = G; aa.V = V; aa.nch = e->acc_nch; aa.chunk = e->acc_chunk;
+        aa.B = pf ? 1 : n; aa.G = pf ? 1 : G; aa.V = V; aa.nch = e->acc_nch; aa.chunk = e->acc_chunk;
         aa.exit_layer = is_exit ? exit_layer : L;
         aa.is_final = is_exit ? 0 : 1;
         aa.ktrace = e->ktrace;
@@ -699,14 +715,18 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             aa.ctx = (const int32_t*)(e->meta_dev + e->off_ctx);
             aa.page_table = (const int32_t*)(e->meta_dev + e->off_pt);
             aa.pt_stride = e->pt_stride;
-            aa.B = n; aa.G = G; aa.n_heads = e->H; aa.head_dim = e->D; aa.d_model = d; aa.n_layers = L;
+            aa.B = nA; aa.G = GA; aa.n_heads = e->H; aa.head_dim = e->D; aa.d_model = d; aa.n_layers = L;
+            if (pf) {
+                aa.g_rows = (const int32_t*)(e->meta_dev + e->off_grows);
+                aa.ctx_pre = (const int32_t*)(e->meta_dev + e->off_cpre);
+            }
             aa.layer = l; aa.page_tokens = e->cfg.page_tokens; aa.nchunk = nchunk;
             aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)e->D));
             aa.ktrace = e->ktrace;
             aa.ktrace_id = nl;
             aa.atrace = e->atrace ? e->atrace + (size_t)l * 16 : nullptr;
             LAUNCH(SV_K_ATTN, l, st, attn_bytes, attn_flops,
-                   e->D == 128 ? attn3_launch(aa, e->attn_splits > 0 ? e->attn_splits : attn3_splits(n, e->H, nchunk, e->num_sms), max_ctx, st)
+                   e->D == 128 ? attn3_launch(aa, e->attn_splits > 0 ? e->attn_splits : attn3_splits(nA, e->H, nchunk, e->num_sms), max_ctx, st)
                                : attn_launch(aa, st));
         }
         {   // O projection + residual
@@ -1234,6 +1254,79 @@ extern "C" sv_status sv_ticket_release(sv_ticket* t) {
     cudaEventDestroy(t->ev_done);
     delete t;
     return SV_OK;
+}
+
+// ------------------------------------------------------------------ prefill
+// append a prompt of n tokens to the session's KV cache in
+// one pass (query blocks of 16 rows (8 if head_dim != 128) as attention requests
+// over the shared page table, causal inside the prompt) and emit the next token
+// from the last row (argmax, or a race sample of p with the session's Philox
+// stream at round_id = last_round + 1).  Synchronous, no CUDA graph.
+extern "C" sv_status sv_prefill(sv_session* s, const int32_t* tokens, int32_t n, int32_t sample,
+                                sv_exit_result* out) {
+    if (!s || !tokens || !out || n < 1) return fail(SV_E_INVALID, "bad arguments");
+    sv_engine* e = s->e;
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (e->poisoned) return fail(SV_E_DEVICE, "engine poisoned by an earlier CUDA error");
+    if (e->inflight || s->busy) return fail(SV_E_BUSY, "a ticket is in flight");
+    if (e->opts.fused) return fail(SV_E_INVALID, "prefill runs on the per-op engine");
+    if (n > e->opts.max_prefill) return fail(SV_E_CAPACITY, "n > max_prefill");
+    for (int i = 0; i < n; ++i)
+        if (tokens[i] < 0 || tokens[i] >= e->V) return fail(SV_E_INVALID, "token out of range");
+    const int gb = e->D == 128 ? 16 : 8, nq = (n + gb - 1) / gb;
+    const int len = s->len;
+    if (len + nq * gb > e->cfg.max_ctx || !ensure_blocks(e, s, len + nq * gb))
+        return fail(SV_E_CAPACITY, "kv capacity");
+    CK(cudaSetDevice(e->device));
+    uint8_t* mh = e->meta_host;
+    int32_t* tok = (int32_t*)(mh + e->off_tok);
+    int32_t* pos = (int32_t*)(mh + e->off_pos);
+    int32_t* rreq = (int32_t*)(mh + e->off_req);
+    int32_t* ctxa = (int32_t*)(mh + e->off_ctx);
+    int32_t* pt = (int32_t*)(mh + e->off_pt);
+    int32_t* grows = (int32_t*)(mh + e->off_grows);
+    int32_t* cpre = (int32_t*)(mh + e->off_cpre);
+    for (int i = 0; i < n; ++i) {
+        tok[i] = tokens[i];
+        pos[i] = len + i;
+        rreq[i] = i / gb;
+    }
+    for (int b = 0; b < nq; ++b) {
+        ctxa[b] = len + b * gb;
+        grows[b] = std::min(gb, n - b * gb);
+        cpre[b] = len;
+        for (size_t k = 0; k < s->blocks.size(); ++k) pt[b * e->pt_stride + k] = s->blocks[k];
+    }
+    ReqDev* rd = (ReqDev*)(mh + e->off_reqdev);
+    memset(rd, 0, sizeof(ReqDev));
+    rd->philox_seed = s->seed;
+    rd->session_id = (uint32_t)s->id;
+    rd->round_id = s->last_round + 1;
+    rd->ctx = len;
+    rd->probs = sample ? (uint64_t)e->logits_final : 0;   // gamma = 0: never read, non-zero = sample
+    cudaStream_t st = e->s_cap;
+    CK(cudaMemcpyAsync(e->meta_dev, e->meta_host, e->meta_bytes, cudaMemcpyHostToDevice, st));
+    e->pf.on = true;
+    e->pf.n_tokens = n;
+    e->pf.nq = nq;
+    e->pf.gb = gb;
+    int nl = 0;
+    const int nchunk = std::min(e->max_nchunk, (len + n + 63) / 64);
+    cudaError_t r = issue_step(e, st, 1, 0, 0ull, nchunk, &nl);
+    e->pf.on = false;
+    if (r == cudaSuccess) r = cudaMemcpyAsync(out, e->res_final_dev, sizeof(sv_exit_result), cudaMemcpyDeviceToHost, st);
+    if (r == cudaSuccess) r = cudaStreamSynchronize(st);
+    if (r != cudaSuccess) {
+        e->poisoned = true;
+        return fail(SV_E_DEVICE, std::string("prefill: ") + cudaGetErrorString(r));
+    }
+    e->last_launches = nl;
+    if (out->status == SV_OK) {
+        s->len = len + n;
+        s->last_round = out->round_id;
+        out->new_len = s->len;
+    }
+    return (sv_status)out->status;
 }
 
 extern "C" sv_status sv_verify(sv_session* s, const sv_verify_req* req, int32_t exit_layer, sv_exit_result* early,

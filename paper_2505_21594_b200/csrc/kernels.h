@@ -92,6 +92,11 @@ struct AttnArgs {
     unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
     int ktrace_id = 0;
     unsigned long long* atrace = nullptr;   // optional phase stamps of CTAs (0,0) and (0,last) [16] (SV_ATRACE)
+    // prefill (query blocks of one session as G-row "requests"): valid rows of each
+    // request (nullptr: G) and the rows cached before the step (nullptr: ctx), i.e.
+    // the rows that may be loaded before griddepcontrol.wait
+    const int32_t* g_rows = nullptr;
+    const int32_t* ctx_pre = nullptr;
 };
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st);
 // v3 (head_dim 128): mma.sync bf16 tensor-core tiles, per-warp cp.async rings,

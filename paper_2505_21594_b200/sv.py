@@ -40,7 +40,7 @@ class sv_weights(C.Structure):
 
 class sv_engine_opts(C.Structure):
     _fields_ = [("max_batch", C.c_int32), ("max_gamma", C.c_int32), ("use_graphs", C.c_int32),
-                ("fused", C.c_int32)]
+                ("fused", C.c_int32), ("max_prefill", C.c_int32)]
 
 
 class sv_verify_req(C.Structure):
@@ -101,6 +101,7 @@ EXPORTS = {
                                          C.c_int32, C.POINTER(sv_exit_result), C.POINTER(sv_exit_result),
                                          C.c_void_p, C.POINTER(C.c_void_p)]),
     "sv_wait_exit": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
+    "sv_prefill": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.POINTER(sv_exit_result)]),
     "sv_exits_ready": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "sv_wait_early": (C.c_int, [C.c_void_p, C.c_int64]),
     "sv_wait_final": (C.c_int, [C.c_void_p, C.c_int64]),
@@ -236,6 +237,16 @@ class Session:
         check(lib().sv_debug_kv_rows(self.h, layer, first, count, k.ctypes.data, v.ctypes.data))
         return k, v
 
+    def prefill(self, tokens, sample: bool = False):
+        """Append the prompt to the KV cache; returns the sv_exit_result whose
+        tokens[0] is the next token (the pending token of the first verify round)."""
+        t = np.ascontiguousarray(np.asarray(tokens, dtype=np.int32))
+        out = sv_exit_result()
+        check(lib().sv_prefill(self.h, t.ctypes.data_as(C.POINTER(C.c_int32)), len(t), 1 if sample else 0,
+                               C.byref(out)))
+        self.last_round = out.round_id
+        return out
+
     def close(self):
         if self.h:
             check(lib().sv_session_close(self.h))
@@ -317,7 +328,8 @@ class Ticket:
 
 class Engine:
     def __init__(self, mc, weights: Weights, max_batch: int = 1, max_gamma: int = 8,
-                 kv_blocks: int = None, use_graphs: bool = True, device: int = 0, fused: bool = None):
+                 kv_blocks: int = None, use_graphs: bool = True, device: int = 0, fused: bool = None,
+                 max_prefill: int = 0):
         import torch
         self.mc = mc
         self.device = device
@@ -329,7 +341,7 @@ class Engine:
         self.kv_pool = torch.empty(blk * kv_blocks, dtype=torch.uint8, device=f"cuda:{device}")
         if fused is None:
             fused = os.environ.get("SV_FUSED", "0") == "1"
-        opts = sv_engine_opts(max_batch, max_gamma, 1 if use_graphs else 0, 1 if fused else 0)
+        opts = sv_engine_opts(max_batch, max_gamma, 1 if use_graphs else 0, 1 if fused else 0, max_prefill)
         self.fused = bool(fused)
         h = C.c_void_p()
         check(lib().sv_engine_create(C.byref(self.cfg), C.byref(weights.w), C.byref(opts), device,
