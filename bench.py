@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4", "C5"])
     ap.add_argument("--gamma", type=int, default=4)
     ap.add_argument("--exit-layer", type=int, default=16)
+    ap.add_argument("--prefill", action="store_true",
+                    help="NEXT-2: build each request's cached context with sv_prefill (timed, reported as "
+                         "'prefill') instead of synthetic KV")
     ap.add_argument("--all-exits", action="store_true",
                     help="NEXT-1: an early exit after every layer 1..L-1, streamed (overrides --exit-layer)")
     ap.add_argument("--alpha", type=float, default=0.825)
@@ -323,14 +326,25 @@ def run_ours(args):
         exit_layer = 0
     W = sv.Weights(mc, seed=1, device=local)
     blocks_per = (ctx + gamma + 1 + 63) // 64
-    eng = sv.Engine(mc, W, max_batch=per, max_gamma=max(1, gamma), kv_blocks=per * blocks_per, device=local)
+    eng = sv.Engine(mc, W, max_batch=per, max_gamma=max(1, gamma), kv_blocks=per * blocks_per, device=local,
+                    max_prefill=ctx if args.prefill else 0)
     sessions = []
-    for rid in shard(total, world, rank):          # contiguous shard of the request ids
-        s = eng.open_session(rid + 1, 0x5EED0000 + rid)
-        s.fill_kv(ctx, kv_seed=1000 + rid)
-        sessions.append(s)
-    pend = prefix_tokens(3 + rank, per, mc.vocab)
     rounds = Rounds()
+    pend = prefix_tokens(3 + rank, per, mc.vocab)
+    prefill_s = []
+    for i, rid in enumerate(shard(total, world, rank)):   # contiguous shard of the request ids
+        s = eng.open_session(rid + 1, 0x5EED0000 + rid)
+        if args.prefill:   # synthetic prompt of ctx uniform token ids through the model
+            prompt = np.random.default_rng([5, rid]).integers(0, mc.vocab, size=ctx)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = s.prefill(prompt, sample=True)
+            prefill_s.append(time.perf_counter() - t0)
+            pend[i] = res.emitted()[-1]
+            rounds.r[id(s)] = res.round_id
+        else:
+            s.fill_kv(ctx, kv_seed=1000 + rid)
+        sessions.append(s)
     # N_SETS independent calibrated draft sets per request; step i verifies set i % N_SETS
     n_sets = N_SETS if per <= 16 else 2
     sets = [build_calibrated_drafts(sv, eng, sessions, pend, ctx, gamma, args.alpha, mc.vocab,
@@ -494,6 +508,10 @@ def run_ours(args):
             "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches * args.steps, "kernels_per_step": launches,
+            "prefill": ({"prompt_tokens": ctx, "ms_per_prompt_p50": round(1e3 * statistics.median(prefill_s), 3),
+                         "tokens_per_s": round(ctx / statistics.median(prefill_s), 1),
+                         "note": "sv_prefill, one synchronous call per request, host wall clock"}
+                        if prefill_s else None),
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
     if dist:

@@ -10,6 +10,8 @@ for g in 1 2 3 4 5 6 7 8; do timeout 300 python bench.py --config C3 --gamma $g 
 for e in 8 24; do timeout 300 python bench.py --config C3 --exit-layer $e --steps 20 --warmup 3 --no-cpu-baseline > $OUT/c3_e$e.json 2>/dev/null; done
 timeout 300 python bench.py --all-exits --steps 20 --warmup 3 --no-cpu-baseline > $OUT/c2_all_exits.json 2>/dev/null
 timeout 600 python bench.py --config C5 --steps 10 --warmup 3 --no-cpu-baseline > $OUT/c5.json 2>/dev/null
+timeout 600 python bench.py --config C5 --prefill --steps 10 --warmup 3 --no-cpu-baseline > $OUT/c5_prefill.json 2>/dev/null
+timeout 300 python bench.py --gamma 0 --steps 20 --warmup 3 --no-cpu-baseline > $OUT/c2_ar_gamma0.json 2>/dev/null
 timeout 900 python bench.py --config C4 --steps 5 --warmup 3 --no-cpu-baseline > $OUT/c4.json 2>/dev/null
 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/c2_launches.csv python tools/ncu_step.py > $OUT/ncu_list.log 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"gemm_kernel|attn3" -c 10 -o $OUT/c2_full python tools/ncu_step.py > $OUT/ncu_full.log 2>&1
