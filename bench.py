@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--prefill", action="store_true",
                     help="NEXT-2: build each request's cached context with sv_prefill (timed, reported as "
                          "'prefill') instead of synthetic KV")
+    ap.add_argument("--adapters", type=int, default=0, metavar="RANK",
+                    help="NEXT-3: exit adapters of this rank (e.g. 384) on every early exit")
     ap.add_argument("--all-exits", action="store_true",
                     help="NEXT-1: an early exit after every layer 1..L-1, streamed (overrides --exit-layer)")
     ap.add_argument("--alpha", type=float, default=0.825)
@@ -328,6 +330,8 @@ def run_ours(args):
     blocks_per = (ctx + gamma + 1 + 63) // 64
     eng = sv.Engine(mc, W, max_batch=per, max_gamma=max(1, gamma), kv_blocks=per * blocks_per, device=local,
                     max_prefill=ctx if args.prefill else 0)
+    if args.adapters:
+        eng.set_adapters(sv.Adapters(mc, args.adapters, seed=9, device=local))
     sessions = []
     rounds = Rounds()
     pend = prefix_tokens(3 + rank, per, mc.vocab)
@@ -497,6 +501,7 @@ def run_ours(args):
                                    f"{per} request(s)/GPU, ctx {ctx}, gamma {gamma}, "
                                    + (f"early exits after layers 1..{mc.n_layers - 1} (streamed)" if exit_layers
                                       else f"early exit at layer {exit_layer}")
+                                   + (f", exit adapters rank {args.adapters}" if args.adapters else "")
                                    + f", stochastic acceptance, alpha {args.alpha}",
                        "global_batch": total, "seq_len": ctx, "gamma": gamma,
                        "exit_layer": exit_layers if exit_layers else exit_layer,

@@ -104,6 +104,25 @@ SV_API sv_status sv_weight_sizes(const sv_model_cfg* cfg, size_t* embed, size_t*
 SV_API sv_status sv_weights_generate(const sv_model_cfg* cfg, const sv_weights* w, uint64_t seed,
                               void* stream);
 
+/* Exit adapters (structure only, random init): "adapter
+ * layers after each layer ... Each adapter connects to the LM head",
+ * 101M parameters over 31 exits of Llama2-7B.  Reading (DESIGN.md
+ * R7b): for an early exit after layer l < n_layers the head reads
+ *   A_l(h) = h + silu(RMSNorm(h) * g[l] . w_dn[l]^T) . w_up[l]^T
+ * instead of h^(l).  Arrays [n_layers], entry l-1 = the adapter of layer l (entry
+ * n_layers-1 unused: the final layer keeps the plain head); device bf16:
+ *   w_dn [rank][d], w_up [d][rank], g [d];  rank % 128 == 0. */
+typedef struct {
+    int32_t rank;
+    void** w_dn;
+    void** w_up;
+    void** g;
+} sv_adapters;
+SV_API sv_status sv_adapter_sizes(const sv_model_cfg* cfg, int32_t rank, size_t* dn, size_t* up, size_t* g);
+/* Counter-hash random init of every adapter (bit-identical to oracle/gen.py
+ * adapter_weights); asynchronous on `stream`. */
+SV_API sv_status sv_adapters_generate(const sv_model_cfg* cfg, const sv_adapters* a, uint64_t seed, void* stream);
+
 /* Bytes of one KV block: page_tokens positions of K and V for every layer
  * (layout DESIGN.md "Data layout in HBM": [layer][K|V][head][slot][head_dim] bf16). */
 SV_API size_t sv_kv_block_bytes(const sv_model_cfg* cfg);
@@ -132,6 +151,9 @@ typedef struct {
 SV_API sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights* w, const sv_engine_opts* opts,
                            int device, void* kv_pool, size_t kv_pool_bytes, sv_engine** out);
 SV_API sv_status sv_engine_destroy(sv_engine* e);
+/* Use exit adapters for every early exit (NULL: identity adapters, the plain
+ * head).  The pointers must outlive the engine; invalidates captured graphs. */
+SV_API sv_status sv_engine_set_adapters(sv_engine* e, const sv_adapters* a);
 /* Kernels the last submit launched (graph nodes counted individually). */
 SV_API sv_status sv_engine_last_launches(const sv_engine* e, int32_t* n_kernels);
 

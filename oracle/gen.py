@@ -155,6 +155,30 @@ def global_weights(cfg, seed: int) -> dict:
     )
 
 
+TID_ADAPTER_BASE = 0x200000
+
+
+def adapter_tid(layer: int, kind: int) -> int:
+    """Exit adapter after decoder layer `layer` (1-based): kind 0 = W_dn, 1 = W_up, 2 = gain."""
+    return TID_ADAPTER_BASE + 4 * layer + kind
+
+
+def adapter_sigmas(cfg, rank: int):
+    """W_dn as the other input projections (1.28/sqrt(d)); W_up small (0.1/sqrt(r)) so a
+    random adapter perturbs the exit without swamping h (R7b)."""
+    return dict(dn=1.28 / np.sqrt(cfg.d_model), up=0.1 / np.sqrt(rank), gain=0.1)
+
+
+def adapter_weights(cfg, seed: int, layer: int, rank: int) -> dict:
+    """Exit adapter of layer `layer` (1-based), logical layouts [out, in]:
+    dn [rank][d], up [d][rank], g [d]."""
+    d = cfg.d_model
+    sg = adapter_sigmas(cfg, rank)
+    return dict(dn=gen_tensor(seed, adapter_tid(layer, 0), (rank, d), sg["dn"]),
+                up=gen_tensor(seed, adapter_tid(layer, 1), (d, rank), sg["up"]),
+                g=gen_tensor(seed, adapter_tid(layer, 2), (d,), sg["gain"], offset=1.0))
+
+
 def synthetic_kv(cfg, kv_seed: int, layer: int, length: int):
     """Synthetic cached K and V for positions 0..length-1 of one layer, as float64
     arrays [H, length, Dh] (the bf16 values the cache holds)."""

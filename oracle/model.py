@@ -145,6 +145,25 @@ def forward(model: Model, cache: KVCache, tokens: np.ndarray, exit_layer: int = 
     return lm_head(model, h), exit_logits, hs
 
 
+class Adapters:
+    """Exit adapters, SURVEY.md §8(f) NEXT-3 (structure only, random init): "adapter
+    layers after each layer ... Each adapter connects to the LM head",
+    ~3.26M parameters per exit for Llama2-7B (101M / 31 exits).  Reading
+    (R7b): a residual bottleneck of rank r on h^(l),
+        A_l(h) = h + silu(RMSNorm(h) * g_l  W_dn^T) W_up^T ,
+    whose output goes through the shared final norm + LM head (r = 384 at d = 4096:
+    2 d r + d = 3.15M parameters)."""
+
+    def __init__(self, cfg, seed: int, rank: int, layers):
+        self.cfg, self.rank = cfg, rank
+        self.w = {l: gen.adapter_weights(cfg, seed, l, rank) for l in layers}
+
+    def apply(self, layer: int, h: np.ndarray) -> np.ndarray:
+        w = self.w[layer]
+        x = rms_norm(h, w["g"], self.cfg.rms_eps)
+        return h + silu(x @ w["dn"].T) @ w["up"].T
+
+
 def lm_head(model: Model, h: np.ndarray) -> np.ndarray:
     """z = LMHead(RMSNorm(h) * g_final)  (PAPER.md:101-102)."""
     x = rms_norm(h, model.glob["g_final"], model.cfg.rms_eps)

@@ -42,7 +42,9 @@ class StepOut:
 
 
 def verify_step(model: Model, sess: Session, round_id: int, pending: int, drafts,
-                probs=None, exit_layer: int = 0, exit_layers=()) -> StepOut:
+                probs=None, exit_layer: int = 0, exit_layers=(), adapters=None) -> StepOut:
+    """adapters (oracle.model.Adapters or None): exit adapters applied to h^(l_e)
+    before the shared LM head for every early exit l_e < L (NEXT-3)."""
     cfg = model.cfg
     drafts = [int(x) for x in drafts]
     gamma = len(drafts)
@@ -54,13 +56,16 @@ def verify_step(model: Model, sess: Session, round_id: int, pending: int, drafts
     ctx = sess.cache.length
     block = np.array([pending] + drafts, dtype=np.int64)
     z, ze, hs = forward(model, sess.cache, block, exit_layer)
+    if adapters is not None and exit_layer and exit_layer < cfg.n_layers:
+        ze = lm_head(model, adapters.apply(exit_layer, hs[exit_layer]))
     kw = dict(seed=sess.philox_seed, session_id=sess.session_id, round_id=round_id)
     q = None if probs is None else np.asarray(probs, dtype=np.float64)
     final = acc.accept(z, drafts, q, **kw)
     early = acc.accept(ze, drafts, q, **kw) if ze is not None else None
     exits = []
     for le in exit_layers:                            # h^(le) = hs[le] (output of layer le)
-        zl = lm_head(model, hs[le])
+        hl = adapters.apply(le, hs[le]) if adapters is not None and le < cfg.n_layers else hs[le]
+        zl = lm_head(model, hl)
         exits.append((le, acc.accept(zl, drafts, q, **kw), zl))
     if final.status != acc.OK:
         sess.cache.truncate(ctx)                      # protocol error: KV not advanced

@@ -131,6 +131,35 @@ extern "C" sv_status sv_weights_generate(const sv_model_cfg* c, const sv_weights
     return SV_OK;
 }
 
+static uint64_t adapter_tid(int layer1, int kind) { return 0x200000ull + 4ull * layer1 + kind; }   // layer 1-based
+
+extern "C" sv_status sv_adapter_sizes(const sv_model_cfg* c, int32_t rank, size_t* dn, size_t* up, size_t* g) {
+    sv_status s = check_cfg(c);
+    if (s) return s;
+    if (rank < 128 || rank % 128) return fail(SV_E_INVALID, "adapter rank must be a positive multiple of 128");
+    if (dn) *dn = (size_t)rank * c->d_model * 2;
+    if (up) *up = (size_t)c->d_model * rank * 2;
+    if (g) *g = (size_t)c->d_model * 2;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_adapters_generate(const sv_model_cfg* c, const sv_adapters* a, uint64_t seed, void* stream) {
+    sv_status s = check_cfg(c);
+    if (s) return s;
+    if (!a || !a->w_dn || !a->w_up || !a->g) return fail(SV_E_INVALID, "adapters is NULL");
+    if ((s = sv_adapter_sizes(c, a->rank, nullptr, nullptr, nullptr))) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int d = c->d_model, r = a->rank;
+    for (int l = 1; l < c->n_layers; ++l) {   // entry l-1 = adapter after layer l
+        CK(gen_launch(a->w_dn[l - 1], (uint64_t)r * d, GEN_PLAIN, seed, adapter_tid(l, 0), 0, d,
+                      gen_scale(1.28 / std::sqrt((double)d)), 0.f, st));
+        CK(gen_launch(a->w_up[l - 1], (uint64_t)d * r, GEN_PLAIN, seed, adapter_tid(l, 1), 0, r,
+                      gen_scale(0.1 / std::sqrt((double)r)), 0.f, st));
+        CK(gen_launch(a->g[l - 1], d, GEN_PLAIN, seed, adapter_tid(l, 2), 0, d, gen_scale(0.1), 1.0f, st));
+    }
+    return SV_OK;
+}
+
 // ------------------------------------------------------------------ engine
 // profile mode: every launch bracketed by CUDA events on its own stream
 struct ProfRec {
@@ -185,6 +214,12 @@ struct sv_engine {
     bool no_box = false;                        // env SV_NO_BOX: load full token tiles
     int attn_splits = 0;                        // attention split override (env SV_ATTN_SPLITS; 0 = attn3_splits)
     std::vector<CUtensorMap> wmap128;           // weight maps [qkv L][o L][gu L][down L][lm] (box rows 128)
+    // exit adapters (NEXT-3): weights, maps [dn L][up L], exit-stream buffers
+    int ad_rank = 0;
+    std::vector<void*> ad_g;
+    std::vector<CUtensorMap> ad_maps;
+    float *h_exit = nullptr, *ssq_ad = nullptr;  // h^(l) per exit slot [L][MP][d]; Σh² of A_l(h) [d/128][MP]
+    bf16_raw_t *act_ad = nullptr, *u_ad = nullptr;   // silu(.) [MP][rank]; bf16(A_l(h) * g_final) [MP][d]
     // weights
     void *embed, *lm_head, *norm_final;
     std::vector<void*> w_qkv, w_o, w_gu, w_down, norm_attn, norm_mlp;
@@ -334,6 +369,22 @@ static sv_status engine_alloc(sv_engine* e) {
     return SV_OK;
 }
 
+// activation (B operand) maps with `box` rows: {u, attn_out, act, u_exit} and, with
+// exit adapters, {act_ad, u_ad}
+static bool act_maps(sv_engine* e, int box, std::vector<CUtensorMap>* out) {
+    const int d = e->d;
+    std::vector<CUtensorMap> m(e->ad_rank ? 6 : 4);
+    if (!make_tmap_bf16(&m[0], e->u, e->MP, d, box) || !make_tmap_bf16(&m[1], e->attn_out, e->MP, d, box) ||
+        !make_tmap_bf16(&m[2], e->act, e->MP, e->F, box) ||
+        !make_tmap_bf16(&m[3], e->u_exit, (uint64_t)e->L * e->MP, d, box))
+        return false;
+    if (e->ad_rank &&
+        (!make_tmap_bf16(&m[4], e->act_ad, e->MP, e->ad_rank, box) || !make_tmap_bf16(&m[5], e->u_ad, e->MP, d, box)))
+        return false;
+    *out = m;
+    return true;
+}
+
 static sv_status engine_tmaps(sv_engine* e) {
     const int d = e->d, F = e->F;
     e->tm_qkv.resize(e->L); e->tm_o.resize(e->L); e->tm_gu.resize(e->L); e->tm_down.resize(e->L);
@@ -347,10 +398,8 @@ static sv_status engine_tmaps(sv_engine* e) {
     if (!make_tmap_bf16(&e->tm_lm, e->lm_head, e->V, d, 128)) return fail(SV_E_DEVICE, "tensor map (lm_head)");
     for (int tn : {16, 32, 64, 128, 256}) {
         if (tn > e->MP) continue;
-        std::vector<CUtensorMap> m(4);
-        if (!make_tmap_bf16(&m[0], e->u, e->MP, d, tn) || !make_tmap_bf16(&m[1], e->attn_out, e->MP, d, tn) ||
-            !make_tmap_bf16(&m[2], e->act, e->MP, F, tn) || !make_tmap_bf16(&m[3], e->u_exit, (uint64_t)e->L * e->MP, d, tn))
-            return fail(SV_E_DEVICE, "tensor map (activations)");
+        std::vector<CUtensorMap> m;
+        if (!act_maps(e, tn, &m)) return fail(SV_E_DEVICE, "tensor map (activations)");
         e->tm_act[tn] = m;
     }
     // device copy for the fused kernel: weights [qkv L][o L][gu L][down L][lm], then
@@ -438,6 +487,48 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     return SV_OK;
 }
 
+extern "C" sv_status sv_engine_set_adapters(sv_engine* e, const sv_adapters* ad) {
+    if (!e) return fail(SV_E_INVALID, "NULL engine");
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (e->inflight) return fail(SV_E_BUSY, "a ticket is in flight");
+    if (ad && e->opts.fused) return fail(SV_E_INVALID, "exit adapters run on the per-op engine");
+    CK(cudaSetDevice(e->device));
+    const int L = e->L, d = e->d;
+    if (ad) {
+        sv_status s = sv_adapter_sizes(&e->cfg, ad->rank, nullptr, nullptr, nullptr);
+        if (s) return s;
+        if (!ad->w_dn || !ad->w_up || !ad->g) return fail(SV_E_INVALID, "adapter arrays are NULL");
+        if (ad->rank != e->ad_rank) {   // (re)size the exit-stream buffers
+            cudaFree(e->act_ad);
+            e->act_ad = nullptr;
+            CK(cudaMalloc((void**)&e->act_ad, (size_t)e->MP * ad->rank * 2));
+            CK(cudaMemset(e->act_ad, 0, (size_t)e->MP * ad->rank * 2));
+        }
+        if (!e->h_exit) {
+            CK(cudaMalloc((void**)&e->h_exit, (size_t)L * e->MP * d * 4));
+            CK(cudaMalloc((void**)&e->u_ad, (size_t)e->MP * d * 2));
+            CK(cudaMalloc((void**)&e->ssq_ad, (size_t)(d / 128) * e->MP * 4));
+            CK(cudaMemset(e->h_exit, 0, (size_t)L * e->MP * d * 4));
+            CK(cudaMemset(e->u_ad, 0, (size_t)e->MP * d * 2));
+        }
+        e->ad_rank = ad->rank;
+        e->ad_g.assign(ad->g, ad->g + L);
+        e->wmap128.resize(4 * L + 1 + 2 * L);
+        for (int l = 0; l + 1 < L; ++l)   // entry l = adapter after layer l + 1
+            if (!make_tmap_bf16(&e->wmap128[4 * L + 1 + l], ad->w_dn[l], ad->rank, d, 128) ||
+                !make_tmap_bf16(&e->wmap128[4 * L + 1 + L + l], ad->w_up[l], d, ad->rank, 128))
+                return fail(SV_E_DEVICE, "tensor map (adapters)");
+    } else {
+        e->ad_rank = 0;
+    }
+    for (auto& kv : e->tm_act)
+        if (!act_maps(e, kv.first, &kv.second)) return fail(SV_E_DEVICE, "tensor map (activations)");
+    e->tm_box.clear();
+    for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);   // steps change
+    e->graphs.clear();
+    return SV_OK;
+}
+
 extern "C" sv_status sv_engine_destroy(sv_engine* e) {
     if (!e) return fail(SV_E_INVALID, "NULL engine");
     cudaSetDevice(e->device);
@@ -451,7 +542,8 @@ extern "C" sv_status sv_engine_destroy(sv_engine* e) {
     void* dev[] = {e->h, e->qbuf, e->ssq, e->logits_exit, e->logits_final, e->ws_main, e->ws_exit, e->rope,
                    e->attn_o, e->attn_ml, e->u, e->u_exit, e->attn_out, e->act, e->cnt_main, e->cnt_exit,
                    e->cnt_attn, e->cnt_acc_exit, e->cnt_acc_final, e->stats_exit, e->stats_final, e->race_exit,
-                   e->race_final, e->res_exit_dev, e->res_final_dev, e->meta_dev, e->probs_stage};
+                   e->race_final, e->res_exit_dev, e->res_final_dev, e->meta_dev, e->probs_stage,
+                   e->h_exit, e->ssq_ad, e->act_ad, e->u_ad};
     for (void* p : dev)
         if (p) cudaFree(p);
     cudaFreeHost(e->meta_host);
@@ -642,11 +734,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             const int box = (M + 7) / 8 * 8;
             auto it = e->tm_box.find(box);
             if (it == e->tm_box.end()) {
-                std::vector<CUtensorMap> m(4);
-                if (!make_tmap_bf16(&m[0], e->u, e->MP, d, box) || !make_tmap_bf16(&m[1], e->attn_out, e->MP, d, box) ||
-                    !make_tmap_bf16(&m[2], e->act, e->MP, F, box) ||
-                    !make_tmap_bf16(&m[3], e->u_exit, (uint64_t)e->L * e->MP, d, box))
-                    return cudaErrorInvalidValue;
+                std::vector<CUtensorMap> m;
+                if (!act_maps(e, box, &m)) return cudaErrorInvalidValue;
                 it = e->tm_box.emplace(box, m).first;
             }
             Bp = &it->second[bbuf];
@@ -662,10 +751,11 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         }
         return gemm_launch(epi, tn, A, B, a, s);
     };
+    // slot >= 0: the exit reads u_exit slot `slot`; slot < 0: the adapter output u_ad
     auto lm_and_accept = [&](cudaStream_t s, bool is_exit, int exit_layer, int slot) -> cudaError_t {
         GemmArgs a = base_args(e, pf ? 1 : M);
-        a.ssq_in = ssq_at(e, is_exit ? exit_layer : L, 0);
-        a.b_row0 = is_exit ? slot * e->MP : 0;
+        a.ssq_in = (is_exit && slot < 0) ? e->ssq_ad : ssq_at(e, is_exit ? exit_layer : L, 0);
+        a.b_row0 = (is_exit && slot >= 0) ? slot * e->MP : 0;
         if (pf) {   // prefill: the LM head of the last prompt row only (its next token)
             a.b_row0 = e->pf.n_tokens - 1;
             a.ssq_in += e->pf.n_tokens - 1;
@@ -673,7 +763,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         a.logits = is_exit ? e->logits_exit : e->logits_final;
         cudaError_t q;
         LAUNCH(is_exit ? SV_K_LM_EXIT : SV_K_LM_FINAL, -1, s, gemm_bytes(V, d, (double)M * V * 4),
-               2.0 * M * V * d, gemm(EPI_LOGITS, 4 * L, is_exit ? 3 : 0, V, d, a, s, is_exit));
+               2.0 * M * V * d, gemm(EPI_LOGITS, 4 * L, is_exit ? (slot < 0 ? 5 : 3) : 0, V, d, a, s, is_exit));
         AcceptArgs aa = {};
         aa.logits = a.logits;
         aa.req = (const ReqDev*)(e->meta_dev + e->off_reqdev);
@@ -747,9 +837,11 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             a.h = e->h;
             a.g_out = (l + 1 < L) ? e->norm_attn[l + 1] : e->norm_final;
             a.u_out = e->u;
-            if (is_exit_l) {
-                a.g_out2 = e->norm_final;
+            if (is_exit_l) {   // exit copy: bf16(h * g) for the head, or for the adapter (+ fp32 h)
+                const bool ad = e->ad_rank > 0 && l + 1 < L;
+                a.g_out2 = ad ? e->ad_g[l] : e->norm_final;
                 a.u_out2 = e->u_exit + (size_t)exit_k * e->MP * d;
+                if (ad) a.h_out2 = e->h_exit + (size_t)exit_k * e->MP * d;
             }
             a.ssq_out = ssq_at(e, l + 1, 0);
             LAUNCH(SV_K_DOWN, l, st, gemm_bytes(d, F, Md * (is_exit_l ? 12 : 10) + (d / 128) * M * 4.0),
@@ -759,7 +851,25 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         if (is_exit_l) {   // fork early exit k (S10-S11), streamed to mailbox row k
             if ((r = cudaEventRecord(e->ev_fork, st)) != cudaSuccess) return r;
             if ((r = cudaStreamWaitEvent(e->s_exit, e->ev_fork, 0)) != cudaSuccess) return r;
-            if ((r = lm_and_accept(e->s_exit, true, l + 1, exit_k)) != cudaSuccess) return r;
+            if (e->ad_rank > 0 && l + 1 < L) {   // NEXT-3: A_l(h) = h + silu(RMSNorm(h) g W_dn^T) W_up^T
+                const int R = e->ad_rank;
+                GemmArgs g1 = base_args(e, M);
+                g1.ssq_in = ssq_at(e, l + 1, 0);
+                g1.b_row0 = exit_k * e->MP;
+                g1.act = e->act_ad;
+                LAUNCH(SV_K_LM_EXIT, l, e->s_exit, gemm_bytes(R, d, (double)M * R * 2), 2.0 * M * R * d,
+                       gemm(EPI_SILU, 4 * L + 1 + l, 3, R, d, g1, e->s_exit, true));
+                GemmArgs g2 = base_args(e, M);
+                g2.h = e->h_exit + (size_t)exit_k * e->MP * d;
+                g2.g_out = e->norm_final;
+                g2.u_out = e->u_ad;
+                g2.ssq_out = e->ssq_ad;
+                LAUNCH(SV_K_LM_EXIT, l, e->s_exit, gemm_bytes(d, R, Md * 10), 2.0 * M * d * R,
+                       gemm(EPI_RESID, 4 * L + 1 + L + l, 4, d, R, g2, e->s_exit, true));
+                if ((r = lm_and_accept(e->s_exit, true, l + 1, -1)) != cudaSuccess) return r;
+            } else if ((r = lm_and_accept(e->s_exit, true, l + 1, exit_k)) != cudaSuccess) {
+                return r;
+            }
             if ((r = cudaMemcpyAsync(e->mb_exit + (size_t)exit_k * e->opts.max_batch, e->res_exit_dev,
                                      (size_t)n * sizeof(sv_exit_result), cudaMemcpyDeviceToHost, e->s_exit)) !=
                 cudaSuccess)

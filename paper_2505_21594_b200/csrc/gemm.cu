@@ -341,6 +341,7 @@ static cudaError_t launch_epi(int epi, const CUtensorMap& tmA, const CUtensorMap
         case EPI_RESID: return launch_t<TN, EPI_RESID>(tmA, tmB, a, st);
         case EPI_SWIGLU: return launch_t<TN, EPI_SWIGLU>(tmA, tmB, a, st);
         case EPI_LOGITS: return launch_t<TN, EPI_LOGITS>(tmA, tmB, a, st);
+        case EPI_SILU: return launch_t<TN, EPI_SILU>(tmA, tmB, a, st);
     }
     return cudaErrorInvalidValue;
 }

@@ -210,6 +210,7 @@ static cudaError_t big_epi(int epi, const CUtensorMap& tmA, const CUtensorMap& t
         case EPI_RESID: return big_t<TN, EPI_RESID>(tmA, tmB, a, st);
         case EPI_SWIGLU: return big_t<TN, EPI_SWIGLU>(tmA, tmB, a, st);
         case EPI_LOGITS: return big_t<TN, EPI_LOGITS>(tmA, tmB, a, st);
+        case EPI_SILU: return big_t<TN, EPI_SILU>(tmA, tmB, a, st);
     }
     return cudaErrorInvalidValue;
 }

@@ -8,6 +8,7 @@
 //                copy with the final gain); sum(h^2) of the 128-column tile
 //   EPI_SWIGLU : act = bf16(silu(gate * rstd) * (up * rstd)) (64-row interleave)
 //   EPI_LOGITS : z = out * rstd (fp32 logits; LM head)
+//   EPI_SILU   : act = bf16(silu(out * rstd)), row stride N (exit adapter W_dn)
 // 128 threads, r = 0..127 (row of the tile); `sync` = barrier of those threads.
 #pragma once
 #include "common.cuh"
@@ -98,6 +99,7 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
                 hv[j] += sOut[j * TM + r];
                 a.h[idx] = hv[j];
                 reinterpret_cast<bf16*>(a.u_out)[idx] = __float2bfloat16_rn(hv[j] * g);
+                if (a.h_out2) a.h_out2[idx] = hv[j];
                 if (a.u_out2) reinterpret_cast<bf16*>(a.u_out2)[idx] = __float2bfloat16_rn(hv[j] * g2);
             }
             const float sq = warp_sum(hv[j] * hv[j]);
@@ -119,6 +121,13 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
             const float u = sOut[j * TM + 64 + rr] * rs;
             const float y = g / (1.0f + expf(-g)) * u;
             reinterpret_cast<bf16*>(a.act)[(size_t)tok * a.d_ff + nt * 64 + rr] = __float2bfloat16_rn(y);
+        }
+    } else if constexpr (EPI == EPI_SILU) {
+        for (int j = 0; j < EPI_CHUNK; ++j) {
+            const int tok = tok0 + j;
+            if (tok >= a.M) break;
+            const float x = sOut[j * TM + r] * sR[tok - m0];
+            reinterpret_cast<bf16*>(a.act)[(size_t)tok * a.N + n0 + r] = __float2bfloat16_rn(x / (1.0f + expf(-x)));
         }
     } else {  // EPI_LOGITS
         for (int j = 0; j < EPI_CHUNK; ++j) {

@@ -15,7 +15,7 @@ typedef uint16_t bf16_raw_t;   // raw bf16 storage in host-visible structs
 extern bool g_use_pdl;
 
 // ----------------------------------------------------------------- GEMM (K1)
-enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_LOGITS = 3 };
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_LOGITS = 3, EPI_SILU = 4 };
 
 // Per-step request metadata, device resident (one H2D per step).
 struct StepMeta {
@@ -52,6 +52,7 @@ struct GemmArgs {
     const void* g_out2;   // bf16 [d] or nullptr (early-exit copy with the final gain)
     void* u_out2;
     float* ssq_out;       // [d/128][MP] per-tile sum of h^2
+    float* h_out2;        // fp32 [MP][d] copy of the new residual or nullptr (exit adapter input)
     // EPI_SWIGLU
     void* act;            // bf16 [MP][d_ff]
     int d_ff;

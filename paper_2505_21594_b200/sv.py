@@ -38,6 +38,11 @@ class sv_weights(C.Structure):
                 ("norm_attn", C.POINTER(C.c_void_p)), ("norm_mlp", C.POINTER(C.c_void_p))]
 
 
+class sv_adapters(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("w_dn", C.POINTER(C.c_void_p)), ("w_up", C.POINTER(C.c_void_p)),
+                ("g", C.POINTER(C.c_void_p))]
+
+
 class sv_engine_opts(C.Structure):
     _fields_ = [("max_batch", C.c_int32), ("max_gamma", C.c_int32), ("use_graphs", C.c_int32),
                 ("fused", C.c_int32), ("max_prefill", C.c_int32)]
@@ -101,6 +106,9 @@ EXPORTS = {
                                          C.c_int32, C.POINTER(sv_exit_result), C.POINTER(sv_exit_result),
                                          C.c_void_p, C.POINTER(C.c_void_p)]),
     "sv_wait_exit": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
+    "sv_adapter_sizes": (C.c_int, [C.POINTER(sv_model_cfg), C.c_int32] + [C.POINTER(C.c_size_t)] * 3),
+    "sv_adapters_generate": (C.c_int, [C.POINTER(sv_model_cfg), C.POINTER(sv_adapters), C.c_uint64, C.c_void_p]),
+    "sv_engine_set_adapters": (C.c_int, [C.c_void_p, C.POINTER(sv_adapters)]),
     "sv_prefill": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.POINTER(sv_exit_result)]),
     "sv_exits_ready": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "sv_wait_early": (C.c_int, [C.c_void_p, C.c_int64]),
@@ -207,6 +215,33 @@ class Weights:
         n = int(np.prod(shapes[name]))
         off = ptr - self.buf.data_ptr()
         return self.buf[off:off + 2 * n].view(torch.bfloat16).view(*shapes[name])
+
+
+class Adapters:
+    """Exit adapters (NEXT-3, structure only): device bf16 weights in one torch
+    allocation, filled by sv_adapters_generate (bit-identical to oracle/gen.py)."""
+
+    def __init__(self, mc, rank: int, seed: int, device: int = 0):
+        import torch
+        self.mc, self.rank = mc, rank
+        cfg = make_cfg(mc)
+        sz = [C.c_size_t() for _ in range(3)]
+        check(lib().sv_adapter_sizes(C.byref(cfg), rank, *[C.byref(x) for x in sz]))
+        dn, up, g = [x.value for x in sz]
+        al = lambda x: (x + 255) // 256 * 256
+        L = mc.n_layers
+        self.buf = torch.empty(L * (al(dn) + al(up) + al(g)), dtype=torch.uint8, device=f"cuda:{device}")
+        base = self.buf.data_ptr()
+        arr = {k: (C.c_void_p * L)() for k in ("dn", "up", "g")}
+        off = 0
+        for l in range(L):
+            for k, n in (("dn", dn), ("up", up), ("g", g)):
+                arr[k][l] = base + off
+                off += al(n)
+        self._arr = arr
+        self.a = sv_adapters(rank, arr["dn"], arr["up"], arr["g"])
+        check(lib().sv_adapters_generate(C.byref(cfg), C.byref(self.a), seed, _stream_handle(None)))
+        torch.cuda.synchronize()
 
 
 class Session:
@@ -403,6 +438,11 @@ class Engine:
         recs = [dict(kind=KERNEL_KINDS[out[i].kind], layer=out[i].layer, ms=out[i].ms, bytes=out[i].bytes,
                      flops=out[i].flops) for i in range(min(k.value, cap))]
         return [final[i] for i in range(n)], recs
+
+    def set_adapters(self, adapters):
+        """Exit adapters for every early exit (None: the plain shared head)."""
+        self._adapters = adapters
+        check(lib().sv_engine_set_adapters(self.h, C.byref(adapters.a) if adapters is not None else None))
 
     def last_launches(self) -> int:
         n = C.c_int32()

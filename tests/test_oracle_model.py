@@ -159,3 +159,28 @@ def test_synthetic_cache_roundtrip():
     assert np.array_equal(c.k[1], K) and c.length == 20
     c.truncate(7)
     assert c.k[0].shape[1] == 7 and c.length == 7
+
+
+def test_exit_adapter_against_torch_modules_and_identity():
+    """NEXT-3 exit adapter (oracle.model.Adapters, R7b) against the same
+    composition built from library modules in float64 (HF LlamaRMSNorm, torch Linear,
+    SiLU), and the W_up = 0 special case (identity: the exit equals the plain exit)."""
+    import torch
+    from transformers.models.llama.modeling_llama import LlamaRMSNorm
+    cfg = tiny()
+    ad = om.Adapters(cfg, seed=3, rank=128, layers=[1])
+    w = ad.w[1]
+    h = np.random.default_rng(0).standard_normal((5, cfg.d_model)) * 2.0
+    norm = LlamaRMSNorm(cfg.d_model, eps=cfg.rms_eps).double()
+    dn = torch.nn.Linear(cfg.d_model, 128, bias=False).double()
+    up = torch.nn.Linear(128, cfg.d_model, bias=False).double()
+    with torch.no_grad():
+        norm.weight.copy_(torch.from_numpy(w["g"]))
+        dn.weight.copy_(torch.from_numpy(w["dn"]))
+        up.weight.copy_(torch.from_numpy(w["up"]))
+        ht = torch.from_numpy(h)
+        ref = (ht + up(torch.nn.functional.silu(dn(norm(ht))))).numpy()
+    assert np.allclose(ad.apply(1, h), ref, rtol=1e-6, atol=1e-6)   # HF RMSNorm computes its variance in fp32
+    assert not np.allclose(ad.apply(1, h), h)            # a random adapter does act
+    w["up"] = np.zeros_like(w["up"])
+    assert np.array_equal(ad.apply(1, h), h)
