@@ -155,6 +155,8 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
         ++pre;
     }
     pdl_wait();
+    if (tid == 32 && a.pf_ptr)   // the QKV GEMM is done: pull the O weights into L2 while HBM is idle
+        cta_prefetch_l2(a.pf_ptr, a.pf_bytes, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y);
     A3_STAMP(2);
     for (int it = pre; it < NST && it < n_my; ++it) issue(warp + A3_WARPS * it, it);
 

@@ -57,6 +57,21 @@ __device__ __forceinline__ void tma_prefetch_l2_2d(const void* map, int c0, int 
                  "r"(c0), "r"(c1)
                  : "memory");
 }
+// contiguous bytes -> L2 (bulk prefetch; size multiple of 16, address 16-aligned)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+                 : "memory");
+}
+// this CTA's share of [ptr, ptr + bytes) -> L2, in 64 KB requests (one thread)
+__device__ __forceinline__ void cta_prefetch_l2(const void* ptr, size_t bytes, int cta, int ncta) {
+    if (!ptr || !bytes) return;
+    const size_t per = ((bytes + ncta - 1) / ncta + 15) & ~size_t(15);
+    const size_t b0 = (size_t)cta * per, b1 = b0 + per < bytes ? b0 + per : bytes;
+    for (size_t o = b0; o < b1; o += 65536) {
+        const size_t n = b1 - o < 65536 ? b1 - o : 65536;
+        bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(ptr) + o, (uint32_t)(n & ~size_t(15)));
+    }
+}
 __device__ __forceinline__ void tma_prefetch_desc(const void* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

@@ -212,6 +212,7 @@ struct sv_engine {
     int device, num_sms;
     int pf_depth = 0;                           // GemmArgs::pf_depth (env SV_PF)
     bool no_box = false;                        // env SV_NO_BOX: load full token tiles
+    bool attn_pf = false;                       // attention prefetches the O weights to L2 (env SV_ATTN_PF; measured slower)
     int attn_splits = 0;                        // attention split override (env SV_ATTN_SPLITS; 0 = attn3_splits)
     std::vector<CUtensorMap> wmap128;           // weight maps [qkv L][o L][gu L][down L][lm] (box rows 128)
     // exit adapters (NEXT-3): weights, maps [dn L][up L], exit-stream buffers
@@ -457,6 +458,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (getenv("SV_ATTN_RING2")) g_attn_ring1 = false;
     if (getenv("SV_SPLIT_ANY")) g_split_any = true;
     if (getenv("SV_NO_BOX")) e->no_box = true;
+    if (getenv("SV_ATTN_PF")) e->attn_pf = true;
     e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
     e->L = cfg->n_layers; e->d = cfg->d_model; e->F = cfg->d_ff; e->V = cfg->vocab;
     e->H = cfg->n_heads; e->D = cfg->head_dim;
@@ -815,6 +817,10 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             aa.ktrace = e->ktrace;
             aa.ktrace_id = nl;
             aa.atrace = e->atrace ? e->atrace + (size_t)l * 16 : nullptr;
+            if (e->attn_pf) {
+                aa.pf_ptr = e->w_o[l];
+                aa.pf_bytes = (size_t)d * d * 2;
+            }
             LAUNCH(SV_K_ATTN, l, st, attn_bytes, attn_flops,
                    e->D == 128 ? attn3_launch(aa, e->attn_splits > 0 ? e->attn_splits : attn3_splits(nA, e->H, nchunk, e->num_sms), max_ctx, st)
                                : attn_launch(aa, st));

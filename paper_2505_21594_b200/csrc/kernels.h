@@ -98,6 +98,10 @@ struct AttnArgs {
     // the rows that may be loaded before griddepcontrol.wait
     const int32_t* g_rows = nullptr;
     const int32_t* ctx_pre = nullptr;
+    // L2 prefetch of the next GEMM's weights (the O projection), issued once the
+    // QKV GEMM has completed: attention is latency-bound and leaves HBM idle
+    const void* pf_ptr = nullptr;
+    size_t pf_bytes = 0;
 };
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st);
 // v3 (head_dim 128): mma.sync bf16 tensor-core tiles, per-warp cp.async rings,

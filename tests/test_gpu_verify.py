@@ -311,3 +311,44 @@ def test_7b_width_c5_batch(svlib):
     for s in ss:
         s.close()
     eng.close()
+
+
+def test_7b_width_c4_batch(svlib):
+    """configs[3]-shaped batch on one GPU at the Llama2-7B layer widths (2 layers):
+    B = 256 requests x 5 = 1280 query rows (persistent 128 x 256 GEMM tiles, five
+    token tiles, the batched attention grid), ctx 1024; sampled requests
+    {0, 131, 255} against the fp64 oracle, one stochastic round with an early exit."""
+    from paper_2505_21594_b200 import sv
+    mc = ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=1088)
+    B, gamma, ctx = 256, 4, 1024
+    W = sv.Weights(mc, seed=1)
+    eng = sv.Engine(mc, W, max_batch=B, max_gamma=gamma, kv_blocks=B * 17)
+    model = om.Model(mc, seed=1)
+    ss = []
+    for b in range(B):
+        s = eng.open_session(100 + b, 300 + b)
+        s.fill_kv(ctx, kv_seed=400 + b)
+        ss.append(s)
+    x, q = wd.timing_drafts(34, B, gamma, mc.vocab, s=1.1)
+    qd = torch.from_numpy(q).cuda()
+    t = eng.submit([sv.Request(ss[b], 1, (7 * b) % mc.vocab, x[b], qd[b]) for b in range(B)], exit_layer=1)
+    early = t.wait_early()
+    final = t.wait_final()
+    zf = t.logits(1, gamma).cpu().numpy()
+    ze = t.logits(0, gamma).cpu().numpy()
+    t.release()
+    tally = Tally()
+    for b in (0, 131, 255):
+        osess = oracle_session(mc, model, 100 + b, 300 + b, 400 + b, ctx)
+        out = verify_step(model, osess, 1, (7 * b) % mc.vocab, x[b], q[b].astype(np.float64), exit_layer=1)
+        rel, eps = row_rel_err(zf[b], out.final_logits)
+        rel_e, eps_e = row_rel_err(ze[b], out.exit_logits)
+        assert rel.max() < LOGIT_TOL and rel_e.max() < LOGIT_TOL
+        tally.add(out.final, final[b], decision_bound(eps.max()), tag=("final", b))
+        tally.add(out.early, early[b], decision_bound(eps_e.max()), tag=("exit", b))
+        assert ss[b].length == final[b].new_len
+    print(tally.report())
+    assert not tally.hard_mismatch
+    for s in ss:
+        s.close()
+    eng.close()
