@@ -21,6 +21,7 @@
 // Numerics: q and p are rounded to bf16 for the MMA (as in a bf16 model); scores,
 // softmax statistics and O accumulate in fp32.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -393,6 +394,11 @@ static cudaError_t attn3_launch_t(const AttnArgs& a, int splits, cudaStream_t st
         cudaError_t e =
             cudaFuncSetAttribute(attn3_kernel<NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, A3Cfg<NST>::SMEM);
         if (e != cudaSuccess) return e;
+        if (!getenv("SV_NO_CARVEOUT")) {
+            e = cudaFuncSetAttribute(attn3_kernel<NST>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
+            if (e != cudaSuccess) return e;
+        }
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};

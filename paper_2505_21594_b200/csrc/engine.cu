@@ -1025,7 +1025,8 @@ static cudaError_t build_fused_plan(sv_engine* e, int n, int gamma, int exit_lay
     const int s_lm = add(gemm_stage(EPI_LOGITS, e->d_tmaps + 4 * L, tu, V, d, lm, prev, (double)M * V * 4));
     const int s_stats = add(accept_stage(false, s_lm, true));
     add(accept_stage(false, s_stats, false));
-    cudaError_t r = fused_build(P, st, e->num_sms, tn, e->D);
+    const char* cps = getenv("SV_FUSED_CPS");   // CTAs per SM of the persistent grid (library built to fit)
+    cudaError_t r = fused_build(P, st, e->num_sms * (cps ? atoi(cps) : 1), tn, e->D);
     if (r != cudaSuccess) return r;
     P->early_host_dev = e->mb_exit_dev;
     P->early_flag_dev = e->mb_flag_dev;

@@ -39,7 +39,10 @@ constexpr int F_BK = 64;
 constexpr int F_TM = 128;
 constexpr int F_A_STAGE = F_TM * F_BK * 2;   // 16 KB of weights per stage
 constexpr int F_THREADS = 192;
-constexpr int F_SMEM_MAX = 232448;           // 227 KB opt-in dynamic shared memory
+#ifndef SV_FUSED_SMEM
+#define SV_FUSED_SMEM 232448                 // 227 KB opt-in dynamic shared memory (one CTA per SM)
+#endif
+constexpr int F_SMEM_MAX = SV_FUSED_SMEM;
 
 template <int TN>
 struct EpiSmem {
@@ -60,12 +63,12 @@ struct FCfg {
     static constexpr int BAR = 512;
     static constexpr int SCACHE = 1024;      // per-item copy of the stage descriptor
     static constexpr int STAGES_RAW = (F_SMEM_MAX - 1024 - UNION - BAR - SCACHE) / STAGE;
-    static constexpr int STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
+    static constexpr int STAGES = STAGES_RAW < 2 ? 2 : (STAGES_RAW > 12 ? 12 : STAGES_RAW);   // (a shallow-smem
+                                                     // build cannot launch the largest tiles: launch error)
     static constexpr int SMEM = 1024 + STAGES * STAGE + UNION + BAR + SCACHE;
     static_assert(sizeof(FStage) <= SCACHE && sizeof(FStage) % 16 == 0, "stage descriptor cache");
     static constexpr int TBUF = TN < 32 ? 32 : TN;                 // TMEM columns per accumulator
     static constexpr int TCOLS = 2 * TBUF <= 32 ? 32 : (2 * TBUF <= 64 ? 64 : (2 * TBUF <= 128 ? 128 : (2 * TBUF <= 256 ? 256 : 512)));
-    static_assert(STAGES >= 2, "ring too shallow");
 };
 
 struct FArgs {
@@ -187,7 +190,7 @@ __device__ __forceinline__ void fused_rstd(const GemmArgs& g, float* sR, float* 
 }
 
 template <int TN, int D>
-__global__ void __launch_bounds__(F_THREADS, 1) fused_step_kernel(const __grid_constant__ FArgs f) {
+__global__ void __launch_bounds__(F_THREADS, F_SMEM_MAX < 120 * 1024 ? 2 : 1) fused_step_kernel(const __grid_constant__ FArgs f) {
     using C = FCfg<TN, D>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -492,7 +495,18 @@ static cudaError_t launch_td(const FArgs& a, int grid, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute(fused_step_kernel<TN, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM);
         if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(fused_step_kernel<TN, D>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
         attr = true;
+        if (getenv("SV_FUSED_DEBUG")) {
+            int nb = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fused_step_kernel<TN, D>, F_THREADS, C::SMEM);
+            cudaFuncAttributes fa;
+            cudaFuncGetAttributes(&fa, fused_step_kernel<TN, D>);
+            fprintf(stderr, "fused<%d,%d>: smem %d (static %zu) regs %d -> %d blocks/SM, grid %d\n", TN, D, C::SMEM,
+                    fa.sharedSizeBytes, fa.numRegs, nb, grid);
+        }
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid, 1, 1);
@@ -501,7 +515,8 @@ static cudaError_t launch_td(const FArgs& a, int grid, cudaStream_t st) {
     cfg.stream = st;
     cudaLaunchAttribute attrs[1];
     attrs[0].id = cudaLaunchAttributeCooperative;   // co-residency of all CTAs (spin waits)
-    attrs[0].val.cooperative = 1;
+    attrs[0].val.cooperative = getenv("SV_FUSED_NONCOOP") ? 0 : 1;   // (experiment: the occupancy API
+                                                                      // under-counts 2-CTA/SM tcgen05 grids)
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, fused_step_kernel<TN, D>, a);

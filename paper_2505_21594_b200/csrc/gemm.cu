@@ -44,6 +44,9 @@ namespace sv {
 constexpr int BK = 64;                      // K elements per stage (one 128 B swizzle row)
 constexpr int TM = 128;                     // weight rows per tile (UMMA M)
 constexpr int A_STAGE = TM * BK * 2;        // 16 KB
+#ifndef SV_GEMM_MAX_STAGES
+#define SV_GEMM_MAX_STAGES 8
+#endif
 #ifndef SV_GEMM_CTAS_PER_SM
 #define SV_GEMM_CTAS_PER_SM 2
 #endif
@@ -58,7 +61,7 @@ struct GemmCfg {
     static constexpr int BUDGET =
         (TN <= 64 ? (228 * 1024) / SV_GEMM_CTAS_PER_SM - 1024 : 225 * 1024) - 1024 - AUX;
     static constexpr int STAGES_RAW = BUDGET / STAGE;
-    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+    static constexpr int STAGES = STAGES_RAW > SV_GEMM_MAX_STAGES ? SV_GEMM_MAX_STAGES : STAGES_RAW;
     static constexpr int TMEM_COLS = TN < 32 ? 32 : TN;
     static constexpr int SMEM = 1024 + STAGES * STAGE + AUX;
     static_assert(STAGES >= 2, "pipeline too shallow");
@@ -314,6 +317,25 @@ static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
         cudaError_t e = cudaFuncSetAttribute(gemm_kernel<TN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM);
         if (e != cudaSuccess) return e;
+        if (!getenv("SV_NO_CARVEOUT")) {   // let two grids' CTAs share an SM (PDL co-residency)
+            e = cudaFuncSetAttribute(gemm_kernel<TN, EPI>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
+            if (e != cudaSuccess) return e;
+        }
+        if (getenv("SV_GEMM_DEBUG")) {
+            int nb = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gemm_kernel<TN, EPI>, 128, C::SMEM);
+            cudaFuncAttributes fa;
+            cudaFuncGetAttributes(&fa, gemm_kernel<TN, EPI>);
+            int dev = 0, smsm = 0, rsv = 0, optin = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+            cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            fprintf(stderr, "gemm_kernel<%d,%d>: smem %d static %zu regs %d local %zu -> %d blocks/SM "
+                    "(SM smem %d, reserved/block %d, opt-in max %d)\n", TN, EPI, C::SMEM, fa.sharedSizeBytes,
+                    fa.numRegs, fa.localSizeBytes, nb, smsm, rsv, optin);
+        }
         attr_done = true;
     }
     cudaLaunchConfig_t cfg = {};

@@ -1,2 +1,2 @@
 export PYTHONUNBUFFERED=1
-timeout 900 python -m pytest tests/test_gpu_verify.py -x -q -s -k "c4_batch" 2>&1 | tail -4
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
