@@ -133,3 +133,79 @@ def test_accept_protocol_error_zero_draft_mass(svlib):
     assert got[0].status == sv.SV_E_PROTOCOL
     s.close()
     eng.close()
+
+
+def test_gpu_sampler_leviathan_law_chi_square(svlib):
+    """The GPU acceptance kernels as a sampler: over many rounds
+    (fresh Philox counters each) with drafts x_1 ~ q_1, the first emitted token is
+    distributed as the target p_0 = softmax(z_0) (Leviathan's exactness, the rule
+    of Eq. 2 / DESIGN.md R2), and x_1 is accepted with probability sum_v min(p_0, q_1);
+    chi-square / binomial at alpha = 1e-3, bins with expectation < 5 merged."""
+    from scipy import stats
+    from paper_2505_21594_b200 import sv
+    V, B, rounds = 128, 8, 1500
+    mc = ModelCfg(n_layers=1, d_model=128, n_heads=4, d_ff=128, vocab=V, max_ctx=256)
+    eng = sv.Engine(mc, sv.Weights(mc, seed=1), max_batch=B, max_gamma=8)
+    sessions = [eng.open_session(500 + b, 0xABC + 31 * b) for b in range(B)]
+    rng = np.random.default_rng(12)
+    z0 = rng.standard_normal(V) * 2.0
+    z = np.stack([z0, rng.standard_normal(V)]).astype(np.float32)          # rows 0 (scores x_1), 1 (bonus)
+    p0 = np.exp(z0 - z0.max()); p0 /= p0.sum()
+    q1 = np.exp(rng.standard_normal(V) * 2.0); q1 /= q1.sum()
+    q1 = q1.astype(np.float32)
+    zl = torch.from_numpy(np.broadcast_to(z, (B, 2, V)).copy()).cuda()
+    qd = torch.from_numpy(np.broadcast_to(q1[None], (B, 1, V)).copy()).cuda()
+    counts = np.zeros(V)
+    acc = 0
+    for r in range(1, rounds + 1):
+        x = rng.choice(V, size=B, p=q1.astype(np.float64) / q1.sum())
+        got = eng.debug_accept(zl, [sv.Request(sessions[b], r, 0, [int(x[b])], qd[b]) for b in range(B)])
+        for g in got:
+            assert g.status == 0
+            counts[g.emitted()[0]] += 1
+            acc += g.accepted
+    n = B * rounds
+    exp = n * p0
+    big = exp >= 5
+    obs = np.append(counts[big], counts[~big].sum())
+    ex = np.append(exp[big], exp[~big].sum())
+    assert stats.chisquare(obs, ex).pvalue > 1e-3
+    alpha = np.minimum(p0, q1.astype(np.float64)).sum()
+    assert stats.binomtest(acc, n, alpha).pvalue > 1e-3
+    for s in sessions:
+        s.close()
+    eng.close()
+
+
+def test_argument_edge_cases(svlib):
+    """Synchronous argument errors leave every session untouched: empty batch,
+    gamma above the engine's max, batch above max_batch, token ids out of range,
+    the same session twice, a second submit while one is in flight, empty prefill."""
+    from paper_2505_21594_b200 import sv
+    mc = tiny()
+    eng = sv.Engine(mc, sv.Weights(mc, seed=1), max_batch=2, max_gamma=4, max_prefill=8)
+    s1, s2, s3 = (eng.open_session(i, i) for i in (1, 2, 3))
+    for s in (s1, s2, s3):
+        s.fill_kv(10, kv_seed=1)
+    bad = [
+        [],                                                                  # n = 0
+        [sv.Request(s1, 1, 3, [1, 2, 3, 4, 5])],                             # gamma 5 > max_gamma 4
+        [sv.Request(s, 1, 3, [1, 2]) for s in (s1, s2, s3)],                 # n 3 > max_batch 2
+        [sv.Request(s1, 1, mc.vocab, [1, 2])],                               # pending out of range
+        [sv.Request(s1, 1, 3, [1, -1])],                                     # draft out of range
+        [sv.Request(s1, 1, 3, [1, 2]), sv.Request(s1, 1, 3, [1, 2])],        # same session twice
+    ]
+    for reqs in bad:
+        with pytest.raises((sv.SvError, ValueError)):
+            eng.submit(reqs)
+    t = eng.submit([sv.Request(s1, 1, 3, [1, 2])])
+    with pytest.raises(sv.SvError):                                          # one ticket in flight
+        eng.submit([sv.Request(s2, 1, 3, [1, 2])])
+    t.wait_final()
+    t.release()
+    with pytest.raises(sv.SvError):
+        s2.prefill([])
+    assert s2.length == 10 and s3.length == 10 and s1.length in range(11, 14)
+    for s in (s1, s2, s3):
+        s.close()
+    eng.close()

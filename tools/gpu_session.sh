@@ -1,2 +1,2 @@
 export PYTHONUNBUFFERED=1
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_units.py -x -q -k edge 2>&1 | tail -15
