@@ -212,6 +212,7 @@ struct sv_engine {
     int device, num_sms;
     int pf_depth = 0;                           // GemmArgs::pf_depth (env SV_PF)
     bool no_box = false;                        // env SV_NO_BOX: load full token tiles
+    bool no_wave = false;                       // env SV_NO_WAVE: always 256-token tiles above 128 rows
     bool attn_pf = false;                       // attention prefetches the O weights to L2 (env SV_ATTN_PF; measured slower)
     int attn_splits = 0;                        // attention split override (env SV_ATTN_SPLITS; 0 = attn3_splits)
     std::vector<CUtensorMap> wmap128;           // weight maps [qkv L][o L][gu L][down L][lm] (box rows 128)
@@ -458,6 +459,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (getenv("SV_ATTN_RING2")) g_attn_ring1 = false;
     if (getenv("SV_SPLIT_ANY")) g_split_any = true;
     if (getenv("SV_NO_BOX")) e->no_box = true;
+    if (getenv("SV_NO_WAVE")) e->no_wave = true;
     if (getenv("SV_ATTN_PF")) e->attn_pf = true;
     e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
     e->L = cfg->n_layers; e->d = cfg->d_model; e->F = cfg->d_ff; e->V = cfg->vocab;
@@ -729,10 +731,22 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         a.counters = exit_ws ? e->cnt_exit : e->cnt_main;
         a.ktrace = e->ktrace;
         a.ktrace_id = nl;
+        // persistent path (M > 128): wave-aware token tile, 128 or 256 rows, minimising
+        // ceil(tiles / SMs) x tile (C4 at 1 GPU: O / down 160 -> 320 tiles, 2 -> 3 rounds of half size)
+        int tl = tn;
+        if (M > 128 && a.M == M && !e->no_wave && K <= 4096 && N < 16384) {   // (measured: the long-K down
+                                                                                 // projection and the LM head lose)
+            auto cost = [&](int t) {
+                const long long tiles = (long long)(N / 128) * ((M + t - 1) / t);
+                return ((tiles + e->num_sms - 1) / e->num_sms) * (long long)t;
+            };
+            tl = cost(128) < cost(256) ? 128 : 256;
+        }
+        const auto& tmal = e->tm_act[tl];
         const CUtensorMap& A = e->wmap128[wid];
-        a.splits = gemm_pick_splits(N, K, M, tn, e->num_sms);
-        const CUtensorMap* Bp = &tma[bbuf];
-        if (M < tn && !e->no_box) {   // one token tile: load only its real rows
+        a.splits = gemm_pick_splits(N, K, M, tl, e->num_sms);
+        const CUtensorMap* Bp = &tmal[bbuf];
+        if (M < tl && !e->no_box) {   // one token tile: load only its real rows
             const int box = (M + 7) / 8 * 8;
             auto it = e->tm_box.find(box);
             if (it == e->tm_box.end()) {
@@ -751,7 +765,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             a.pf_kb = nK / 64;
             a.pf_depth = e->pf_depth;
         }
-        return gemm_launch(epi, tn, A, B, a, s);
+        return gemm_launch(epi, tl, A, B, a, s);
     };
     // slot >= 0: the exit reads u_exit slot `slot`; slot < 0: the adapter output u_ad
     auto lm_and_accept = [&](cudaStream_t s, bool is_exit, int exit_layer, int slot) -> cudaError_t {
