@@ -18,6 +18,7 @@ namespace sv {
 
 constexpr int EPI_TM = 128;       // weight rows per tile
 constexpr int EPI_CHUNK = 16;     // token columns per epilogue pass
+constexpr int EPI_PAGE = 64;      // KV page size (sv_model_cfg.page_tokens is required to be 64)
 
 // sPos / sBlk (optional, EPI_QKV): position and KV page of token m0 + t, staged in
 // shared memory once per tile (epi_meta) instead of re-gathered per chunk.
@@ -33,6 +34,13 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
         const int col = (n0 % d) + r;
         const int hd = col / D, i = col % D;
         const int rp = r - i + ((i + half) % D);
+        const int ih = i % half;
+        // per-thread part of the KV offset (head, dim, K or V plane); per token:
+        // (block, layer) plane base and slot (integer division by the runtime
+        // sizes kept out of the token loop)
+        const size_t plane = (size_t)a.n_heads * EPI_PAGE * D;
+        const size_t kv_thread = (sec >= 1 ? (size_t)(sec - 1) * plane : 0) + (size_t)hd * EPI_PAGE * D + i;
+        const size_t layer_planes = (size_t)a.layer * 2 * plane, block_stride = (size_t)a.n_layers * 2 * plane;
         const int nv = min(EPI_CHUNK, a.M - tok0);
         // every global load of the chunk is issued before the first store (the loop
         // below would otherwise serialise one memory round trip per token: the
@@ -55,12 +63,12 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
             for (int j = 0; j < EPI_CHUNK; ++j) req[j] = (j < nv) ? a.meta.row_req[tok0 + j] : 0;
 #pragma unroll
             for (int j = 0; j < EPI_CHUNK; ++j)
-                blk[j] = (j < nv) ? a.meta.page_table[req[j] * a.meta.pt_stride + pos[j] / a.page_tokens] : 0;
+                blk[j] = (j < nv) ? a.meta.page_table[req[j] * a.meta.pt_stride + pos[j] / EPI_PAGE] : 0;
         }
         if (sec < 2) {
 #pragma unroll
             for (int j = 0; j < EPI_CHUNK; ++j)
-                cs[j] = (j < nv) ? reinterpret_cast<const float2*>(a.rope_cs)[(size_t)pos[j] * half + (i % half)]
+                cs[j] = (j < nv) ? reinterpret_cast<const float2*>(a.rope_cs)[(size_t)pos[j] * half + ih]
                                  : make_float2(1.f, 0.f);
         }
 #pragma unroll
@@ -76,10 +84,8 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
             if (sec == 0) {
                 a.qbuf[(size_t)tok * d + col] = v;
             } else {
-                const int slot = pos[j] % a.page_tokens;
-                const size_t off = (((size_t)blk[j] * a.n_layers + a.layer) * 2 + (sec - 1)) *
-                                       ((size_t)a.n_heads * a.page_tokens * D) +
-                                   ((size_t)hd * a.page_tokens + slot) * D + i;
+                const int slot = pos[j] & (EPI_PAGE - 1);
+                const size_t off = (size_t)blk[j] * block_stride + layer_planes + kv_thread + (size_t)slot * D;
                 reinterpret_cast<bf16*>(a.kv_pool)[off] = __float2bfloat16_rn(v);
             }
         }
@@ -169,7 +175,7 @@ __device__ __forceinline__ void epi_meta(const GemmArgs& a, int* sPos, int* sBlk
         int p = 0, b = 0;
         if (tok < a.M) {
             p = a.meta.pos[tok];
-            b = a.meta.page_table[a.meta.row_req[tok] * a.meta.pt_stride + p / a.page_tokens];
+            b = a.meta.page_table[a.meta.row_req[tok] * a.meta.pt_stride + p / EPI_PAGE];
         }
         sPos[t] = p;
         sBlk[t] = b;
