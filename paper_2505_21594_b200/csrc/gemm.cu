@@ -75,8 +75,9 @@ struct GemmCtaSync {
 
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const GemmArgs& a, const float* sOut, const float* sR, float* sRed,
-                                          int tok0, int m0, int n0, int nt) {
-    epi_apply<EPI>(a, sOut, sR, sRed, tok0, m0, n0, nt, (int)threadIdx.x, GemmCtaSync{});
+                                          int tok0, int m0, int n0, int nt, const int* sPos, const int* sBlk,
+                                          const float* hpre = nullptr) {
+    epi_apply<EPI>(a, sOut, sR, sRed, tok0, m0, n0, nt, (int)threadIdx.x, GemmCtaSync{}, sPos, sBlk, hpre);
 }
 
 template <int TN, int EPI>
@@ -96,6 +97,8 @@ __global__ void __launch_bounds__(128, 1)
     int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
     float* sR = reinterpret_cast<float*>(aux + 256);          // [TN]
     float* sRed = sR + 256;                                   // [4][EPI_CHUNK]
+    int* sPos = reinterpret_cast<int*>(aux + 1536);           // [TN <= 64] (EPI_QKV token metadata)
+    int* sBlk = sPos + 64;
     float* sOut = reinterpret_cast<float*>(smem);             // [EPI_CHUNK][128], reuses the ring
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -177,8 +180,23 @@ __global__ void __launch_bounds__(128, 1)
     __syncwarp();
     pdl_wait();   // everything below reads data produced by the previous kernel
 
-    // rstd of the RMSNorm folded into this GEMM (fixed summation order)
-    epi_rstd(a, sR, m0, TN, threadIdx.x, blockDim.x);
+    // warps 2-3 (idle during the mainloop) stage what the epilogue needs while the
+    // tensor core still runs: rstd of the folded RMSNorm (fixed summation order) and,
+    // for the QKV epilogue, each token's position and KV page
+    constexpr bool kStageMeta = (EPI == EPI_QKV && TN <= 64);
+    if (warp >= 2) {
+        epi_rstd(a, sR, m0, TN, threadIdx.x - 64, 64);
+        if constexpr (kStageMeta) epi_meta(a, sPos, sBlk, m0, TN, threadIdx.x - 64, 64);
+    }
+    // residual epilogue of a single 16-token tile: this thread's residual column
+    // is loaded before the accumulator is ready (one round trip off the tail)
+    constexpr bool kPreH = (EPI == EPI_RESID && TN == 16);
+    float hpre[16];
+    if constexpr (kPreH) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            hpre[j] = (m0 + j < a.M) ? __ldcg(&a.h[(size_t)(m0 + j) * a.d_model + n0 + threadIdx.x]) : 0.f;
+    }
 
     mbar_wait(done, 0);
     tc_fence_after();
@@ -196,7 +214,8 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) sOut[j * TM + row] = __uint_as_float(r[j]);
             __syncthreads();
-            epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt);
+            epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt, kStageMeta ? sPos : nullptr,
+                               kStageMeta ? sBlk : nullptr, kPreH ? hpre : nullptr);
         } else {
             float* wsp = a.ws + (((size_t)split * NT + nt) * a.MP) * TM;
 #pragma unroll
@@ -252,7 +271,8 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
                 for (int j = 0; j < EPI_CHUNK; ++j) sOut[j * TM + row] = acc[j];
                 __syncthreads();
-                epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt);
+                epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt, kStageMeta ? sPos : nullptr,
+                               kStageMeta ? sBlk : nullptr, kPreH ? hpre : nullptr);
             }
             if (threadIdx.x == 0) a.counters[nt * MT + mt] = 0;
         }

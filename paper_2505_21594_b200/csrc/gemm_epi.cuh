@@ -25,7 +25,8 @@ constexpr int EPI_PAGE = 64;      // KV page size (sv_model_cfg.page_tokens is r
 template <int EPI, class Sync>
 __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, const float* sR, float* sRed,
                                           int tok0, int m0, int n0, int nt, int r, Sync sync,
-                                          const int* sPos = nullptr, const int* sBlk = nullptr) {
+                                          const int* sPos = nullptr, const int* sBlk = nullptr,
+                                          const float* hpre = nullptr) {
     constexpr int TM = EPI_TM;
     const int warp = r >> 5, lane = r & 31;
     if constexpr (EPI == EPI_QKV) {
@@ -97,7 +98,7 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
         float hv[EPI_CHUNK];
 #pragma unroll
         for (int j = 0; j < EPI_CHUNK; ++j)          // all residual loads in flight first
-            hv[j] = (j < nv) ? __ldcg(&a.h[(size_t)(tok0 + j) * d + n0 + r]) : 0.f;
+            hv[j] = hpre ? hpre[j] : ((j < nv) ? __ldcg(&a.h[(size_t)(tok0 + j) * d + n0 + r]) : 0.f);
 #pragma unroll
         for (int j = 0; j < EPI_CHUNK; ++j) {
             if (j < nv) {
