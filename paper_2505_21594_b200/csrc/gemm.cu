@@ -252,17 +252,19 @@ __global__ void __launch_bounds__(128, 1)
                 for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = 0.f;
                 const float* base = a.ws + ((size_t)nt * a.MP + m0 + c0) * TM + row;
                 int q = 0;
-                if (nv <= 8 && a.splits == 8) {   // batch-1 verify (<= 8 rows, 8 splits): one round trip
+                if (nv <= 8 && a.splits <= 8) {   // batch-1 verify (<= 8 rows, <= 8 splits): one round trip
                     float v[8][8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) v[j][u] = (j < nv) ? __ldcg(base + u * sstride + j * TM) : 0.f;
+                        for (int u = 0; u < 8; ++u)
+                            v[j][u] = (j < nv && u < a.splits) ? __ldcg(base + u * sstride + j * TM) : 0.f;
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) acc[j] += v[j][u];   // split order 0..7, as below
-                    q = 8;
+                        for (int u = 0; u < 8; ++u)
+                            if (u < a.splits) acc[j] += v[j][u];   // split order, as below
+                    q = a.splits;
                 }
                 for (; q + 4 <= a.splits; q += 4) {
                     float v[EPI_CHUNK][4];
