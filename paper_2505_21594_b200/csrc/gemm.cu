@@ -237,12 +237,19 @@ __global__ void __launch_bounds__(128, 1)
         // ---------------- split-K through global memory: the last CTA of the tile
         // (atomic ticket) adds the partials in split order (deterministic; measured
         // faster at batch 1 than a cluster DSMEM reduction: C2 3.22 vs 3.34 ms)
-        __threadfence();
+        // CTA barrier + one acq_rel ticket by thread 0 (release covers the CTA's
+        // partial stores through the barrier; acquire for the reducer's loads)
         __syncthreads();
-        if (threadIdx.x == 0) *s_flag = (atomicAdd(&a.counters[nt * MT + mt], 1) == a.splits - 1);
+        if (threadIdx.x == 0) {
+            int old;
+            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                         : "=r"(old)
+                         : "l"(&a.counters[nt * MT + mt])
+                         : "memory");
+            *s_flag = (old == a.splits - 1);
+        }
         __syncthreads();
         if (*s_flag) {
-            __threadfence();
             const size_t sstride = (size_t)NT * a.MP * TM;
             for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
                 if (m0 + c0 >= a.M) break;
