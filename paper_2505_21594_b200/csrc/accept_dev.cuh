@@ -226,12 +226,10 @@ __device__ bool accept_body(const AcceptArgs& a, int b, int c, int tid, AcceptSm
             Race t = S.wrc[0];
             for (int w = 1; w < NT / 32; ++w) t = race_merge(t, S.wrc[w]);
             a.race[(size_t)b * a.nch + c] = RacePart{t.k1, t.k2, t.f1, t.v1, t.fv1, {0, 0, 0}};
-            __threadfence();
-            S.s_last = (atomicAdd(&a.counters[b], 1) == a.nch - 1);
+            S.s_last = (atomic_add_acq_rel(&a.counters[b], 1) == a.nch - 1);
         }
         sync();
         if (!S.s_last || tid != 0) return false;
-        __threadfence();
         const RacePart* rp = a.race + (size_t)b * a.nch;
         Race t{__ldcg(&rp[0].k1), __ldcg(&rp[0].k2), __ldcg(&rp[0].f1), __ldcg(&rp[0].v1), __ldcg(&rp[0].fv1)};
         for (int k = 1; k < a.nch; ++k)

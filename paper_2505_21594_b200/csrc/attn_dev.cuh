@@ -143,12 +143,10 @@ __device__ bool attn_page_body(const AttnArgs& a, int bh, int c, int tid, AttnSm
         a.part_ml[(pbase + tid) * 2 + 0] = S.sM[tid];
         a.part_ml[(pbase + tid) * 2 + 1] = S.sL[tid];
     }
-    __threadfence();
     sync();
-    if (tid == 0) S.s_last = (atomicAdd(&a.counters[bh], 1) == nch_b - 1);
+    if (tid == 0) S.s_last = (atomic_add_acq_rel(&a.counters[bh], 1) == nch_b - 1);
     sync();
     if (!S.s_last) return false;
-    __threadfence();
     // merge the pages of (b, h) in page order: (1) all (m, l) pairs in parallel
     const size_t mbase = (size_t)bh * a.nchunk * G;
     for (int i = tid; i < nch_b * G; i += 128) {

@@ -180,6 +180,15 @@ __device__ __forceinline__ void ktrace_mark(unsigned long long* tr, int id, int 
     }
 }
 
+// ticket for "the last CTA to arrive does the merge": one acq_rel atomic by the
+// calling thread (release: its prior writes and, after a CTA barrier, the CTA's;
+// acquire: the other arrivals' writes for the merge that follows)
+__device__ __forceinline__ int atomic_add_acq_rel(int* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 // ------------------------------------------------------- programmatic launch
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() {

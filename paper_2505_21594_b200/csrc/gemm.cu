@@ -240,14 +240,7 @@ __global__ void __launch_bounds__(128, 1)
         // CTA barrier + one acq_rel ticket by thread 0 (release covers the CTA's
         // partial stores through the barrier; acquire for the reducer's loads)
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int old;
-            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
-                         : "=r"(old)
-                         : "l"(&a.counters[nt * MT + mt])
-                         : "memory");
-            *s_flag = (old == a.splits - 1);
-        }
+        if (threadIdx.x == 0) *s_flag = (atomic_add_acq_rel(&a.counters[nt * MT + mt], 1) == a.splits - 1);
         __syncthreads();
         if (*s_flag) {
             const size_t sstride = (size_t)NT * a.MP * TM;
