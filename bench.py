@@ -276,10 +276,21 @@ def host_cores():
         return os.cpu_count()
 
 
+def _all_host_threads():
+    """The oracle runs on all host cores even under torchrun (which sets
+    OMP_NUM_THREADS=1 for every rank)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=os.cpu_count())
+    except Exception:
+        return None
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    _keep = _all_host_threads()
     per, total, ctx, scaling = workload(args, 1)
     sample = OracleSample(args, ctx)
     times, toks = [], []
@@ -310,11 +321,19 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SV_BENCH_DEVICE / SV_DIST_BACKEND: test hooks to run the multi-rank path with
+    # several ranks on one GPU (gloo for the counter gather; NCCL needs distinct GPUs)
+    if os.environ.get("SV_BENCH_DEVICE") is not None:
+        local = int(os.environ["SV_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("SV_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     from paper_2505_21594_b200 import sv
     from paper_2505_21594_b200.dist import gather_counters, shard
     from workload import llama2_7b
@@ -432,7 +451,8 @@ def run_ours(args):
     _, recs = eng.profile_step(preqs, exit_layer=exit_layer if not exit_layers else exit_layers[len(exit_layers) // 2])
 
     # gather counters over ranks (the only collective)
-    allv = gather_counters([tokens, elapsed, e2e_tok, e2e_el], device="cuda")
+    allv = gather_counters([tokens, elapsed, e2e_tok, e2e_el],
+                           device="cpu" if os.environ.get("SV_DIST_BACKEND", "nccl") != "nccl" else "cuda")
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -481,6 +501,7 @@ def run_ours(args):
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
+        _keep = _all_host_threads()
         sample = OracleSample(args, ctx)
         t32, _ = sample.step()
         cores, desc = host_cores(), sample.describe(t32)

@@ -1,5 +1,7 @@
 export PYTHONUNBUFFERED=1
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for cfg in "X=1" "SV_O_RING=0" "X=2" "SV_O_RING=0"; do env $cfg timeout 900 python bench.py --no-cpu-baseline --steps 30 > gpurun_out/b.json 2>gpurun_out/b.err
-python -c "
-import json; d=json.load(open('gpurun_out/b.json')); r=d['roofline']; print('C2 $cfg', d['latency_p50_ms'], d['value'], r['step_frac_of_peak'])" || tail -3 gpurun_out/b.err; done
+# the multi-rank bench path (sharding, barriers, max-over-ranks timing, counter gather) with
+# two ranks on the one GPU of this box (gloo for the gather; NCCL needs distinct GPUs)
+SV_BENCH_DEVICE=0 SV_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 10 --warmup 3 > gpurun_out/b2.json 2> gpurun_out/b2.err
+tail -c 900 gpurun_out/b2.json; tail -3 gpurun_out/b2.err
+SV_BENCH_DEVICE=0 SV_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --impl reference --gpus 2 --steps 1 --warmup 1 > gpurun_out/b2r.json 2> gpurun_out/b2r.err
+tail -c 300 gpurun_out/b2r.json; tail -2 gpurun_out/b2r.err
