@@ -1,7 +1,6 @@
 export PYTHONUNBUFFERED=1
-# the multi-rank bench path (sharding, barriers, max-over-ranks timing, counter gather) with
-# two ranks on the one GPU of this box (gloo for the gather; NCCL needs distinct GPUs)
-SV_BENCH_DEVICE=0 SV_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 10 --warmup 3 > gpurun_out/b2.json 2> gpurun_out/b2.err
-tail -c 900 gpurun_out/b2.json; tail -3 gpurun_out/b2.err
-SV_BENCH_DEVICE=0 SV_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --impl reference --gpus 2 --steps 1 --warmup 1 > gpurun_out/b2r.json 2> gpurun_out/b2r.err
-tail -c 300 gpurun_out/b2r.json; tail -2 gpurun_out/b2r.err
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/final_c2.json 2> gpurun_out/final_c2.err
+python -c "
+import json; d=json.load(open('gpurun_out/final_c2.json')); r=d['roofline']; print(d['latency_p50_ms'], d['value'], r['frac'], r['step_frac_of_peak'], d['cpu_baseline']['value'], d['cpu_baseline']['cores'], d['e2e'])"
