@@ -34,8 +34,8 @@ constexpr int A3_WARPS = 4;
 constexpr int A3_ROWB = A3_D * 2;    // 256 B per K / V row
 constexpr int A3_CHB = A3_CHUNK * A3_ROWB;              // 8 KB per K (or V) chunk
 constexpr int A3_STAGE = 2 * A3_CHB;                    // K + V
-template <int NST>   // ring stages per warp: 2 (deep contexts) or 1 (<= 1 chunk per warp: 69 KB, so the
-                     // CTA co-resides with a neighbouring GEMM grid under programmatic dependent launch)
+template <int NST>   // ring stages per warp: 1 (default: 69 KB, two CTAs per SM, and the CTA co-resides
+                     // with a neighbouring GEMM grid under programmatic dependent launch); 2, 3 (SV_ATTN_NST)
 struct A3Cfg {
     static constexpr int SMEM = 1024 + A3_WARPS * NST * A3_STAGE /*rings*/ + 16 * A3_ROWB /*Q bf16*/ + 256;
 };
@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
 
     for (int it = 0; it < n_my; ++it) {
         const int ci = warp + A3_WARPS * it, stage = it % NST;
-        if (NST == 2 && it + 1 < n_my)
+        if (NST >= 3 && it + 2 < n_my)          // chunk `it` landed; later stages may still fly
+            cp_wait<2>();
+        else if (NST >= 2 && it + 1 < n_my)
             cp_wait<1>();
         else
             cp_wait<0>();
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
 }
 
 int attn3_splits(int B, int H, int max_pages, int num_sms) {
-    // one CTA (4 warps, ~136 KB smem) per SM and ONE wave: the largest power-of-two
+    // (sized when the ring was 2-stage, one 136 KB CTA per SM) ONE wave of clusters: the largest power-of-two
     // cluster size whose clusters all fit (5-CTA clusters pack badly into the
     // 16-20-SM GPCs: measured 26 of 32 clusters resident -> two waves)
     const int units = B * H;
@@ -427,10 +429,13 @@ static cudaError_t attn3_launch_t(const AttnArgs& a, int splits, cudaStream_t st
 cudaError_t attn3_launch(const AttnArgs& a, int splits, int max_ctx_len, cudaStream_t st) {
     if (a.head_dim != A3_D || a.page_tokens != 64 || a.G > 16 || splits < 1 || splits > 8)
         return cudaErrorInvalidValue;
-    const int pages = (max_ctx_len + a.G + 63) / 64;
-    const int chunks_per_cta = 2 * ((pages + splits - 1) / splits);
-    if (g_attn_ring1 && chunks_per_cta <= A3_WARPS * 2) return attn3_launch_t<1>(a, splits, st);
-    return attn3_launch_t<2>(a, splits, st);
+    // 1-stage ring at every context length: 69 KB, two CTAs (8 warps) per SM, whose
+    // loads overlap each other's tensor-core work — measured C4 45.8 -> 42.9 ms and
+    // C5 8.30 -> 7.88 ms against the 2-stage ring at one CTA (4 warps) per SM
+    (void)max_ctx_len;
+    if (g_attn_nst == 2) return attn3_launch_t<2>(a, splits, st);
+    if (g_attn_nst == 3) return attn3_launch_t<3>(a, splits, st);
+    return attn3_launch_t<1>(a, splits, st);
 }
 
 }  // namespace sv

@@ -212,6 +212,7 @@ struct sv_engine {
     int device, num_sms;
     int pf_depth = 0;                           // GemmArgs::pf_depth (env SV_PF)
     bool no_box = false;                        // env SV_NO_BOX: load full token tiles
+    bool no_t160 = false;                       // env SV_NO_T160: no 160-token persistent tiles
     bool no_wave = false;                       // env SV_NO_WAVE: always 256-token tiles above 128 rows
     bool attn_pf = false;                       // attention prefetches the O weights to L2 (env SV_ATTN_PF; measured slower)
     int attn_splits = 0;                        // attention split override (env SV_ATTN_SPLITS; 0 = attn3_splits)
@@ -398,7 +399,7 @@ static sv_status engine_tmaps(sv_engine* e) {
             return fail(SV_E_DEVICE, "cuTensorMapEncodeTiled failed (weights)");
     }
     if (!make_tmap_bf16(&e->tm_lm, e->lm_head, e->V, d, 128)) return fail(SV_E_DEVICE, "tensor map (lm_head)");
-    for (int tn : {16, 32, 64, 128, 256}) {
+    for (int tn : {16, 32, 64, 128, 160, 256}) {
         if (tn > e->MP) continue;
         std::vector<CUtensorMap> m;
         if (!act_maps(e, tn, &m)) return fail(SV_E_DEVICE, "tensor map (activations)");
@@ -456,10 +457,11 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     CK(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* pf = getenv("SV_PF")) e->pf_depth = atoi(pf);
     if (const char* as = getenv("SV_ATTN_SPLITS")) e->attn_splits = atoi(as);
-    if (getenv("SV_ATTN_RING2")) g_attn_ring1 = false;
+    if (const char* ns = getenv("SV_ATTN_NST")) g_attn_nst = atoi(ns);
     if (getenv("SV_SPLIT_ANY")) g_split_any = true;
     if (getenv("SV_NO_BOX")) e->no_box = true;
     if (getenv("SV_NO_WAVE")) e->no_wave = true;
+    if (getenv("SV_NO_T160")) e->no_t160 = true;
     if (getenv("SV_ATTN_PF")) e->attn_pf = true;
     e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
     e->L = cfg->n_layers; e->d = cfg->d_model; e->F = cfg->d_ff; e->V = cfg->vocab;
@@ -733,14 +735,20 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         a.ktrace_id = nl;
         // persistent path (M > 128): wave-aware token tile, 128 or 256 rows, minimising
         // ceil(tiles / SMs) x tile (C4 at 1 GPU: O / down 160 -> 320 tiles, 2 -> 3 rounds of half size)
+        // 160-token tiles (UMMA N = 160) fill the rounds of M = 640 / 1280 (C4 at 1-2 GPUs)
         int tl = tn;
-        if (M > 128 && a.M == M && !e->no_wave && K <= 4096 && N < 16384) {   // (measured: the long-K down
-                                                                                 // projection and the LM head lose)
+        if (M > 128 && a.M == M && !e->no_wave && N < 16384) {
             auto cost = [&](int t) {
                 const long long tiles = (long long)(N / 128) * ((M + t - 1) / t);
                 return ((tiles + e->num_sms - 1) / e->num_sms) * (long long)t;
             };
-            tl = cost(128) < cost(256) ? 128 : 256;
+            long long best = cost(256);
+            tl = 256;
+            if (!e->no_t160 && gemm_pick_splits(N, K, M, 160, e->num_sms) == 1 && cost(160) < best) {
+                best = cost(160);
+                tl = 160;
+            }
+            if (K <= 4096 && cost(128) < best) tl = 128;   // (measured: the long-K down projection loses at 128)
         }
         const auto& tmal = e->tm_act[tl];
         const CUtensorMap& A = e->wmap128[wid];

@@ -35,7 +35,7 @@ struct GBCfg {
     static constexpr int RAW = (227 * 1024 - 1024 - EPI - AUX) / STAGE;
     static constexpr int STAGES = RAW > 8 ? 8 : RAW;
     static constexpr int SMEM = 1024 + STAGES * STAGE + EPI + AUX;
-    static constexpr int TCOLS = 2 * TN;                  // two accumulators
+    static constexpr int TCOLS = 2 * TN <= 256 ? 256 : 512;   // two accumulators (alloc: power of two)
     static_assert(STAGES >= 3 && TCOLS <= 512, "config");
 };
 
@@ -219,6 +219,7 @@ cudaError_t gemm_big_launch(int epi, int tile_n, const CUtensorMap& tmA, const C
                             cudaStream_t st) {
     if (tile_n == 128) return big_epi<128>(epi, tmA, tmB, a, st);
     if (tile_n == 256) return big_epi<256>(epi, tmA, tmB, a, st);
+    if (tile_n == 160) return big_epi<160>(epi, tmA, tmB, a, st);
     return cudaErrorInvalidValue;
 }
 
