@@ -20,6 +20,7 @@
 //   memory in rank order -> deterministic.
 // Numerics: q and p are rounded to bf16 for the MMA (as in a bf16 model); scores,
 // softmax statistics and O accumulate in fp32.
+#include <cmath>
 #include <cfloat>
 #include <cstdlib>
 
@@ -90,8 +91,10 @@ __device__ __forceinline__ float ld_dsmem3(const void* p, uint32_t rank) {
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(_t));                                         \
         a.atrace[(blockIdx.y == 0 ? 0 : 8) + (k)] = _t;                                               \
     }
-template <int NST>
-__global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ AttnArgs a) {
+// MINB = CTAs per SM the registers are budgeted for: 3 (<= 168 registers, three 69 KB
+// CTAs = 12 warps per SM) or 2 (~245 registers, no spills)
+template <int NST, int MINB>
+__global__ void __launch_bounds__(128, MINB) attn3_kernel(const __grid_constant__ AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t s_ring = smem_u32(smem);                                   // [warp][stage][K|V] 8 KB tiles
@@ -182,14 +185,6 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
     __syncthreads();
     A3_STAMP(3);
 
-    // Q A-fragments for the 8 k-steps
-    uint32_t qa[8][4];
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-        const int row = (lane & 7) + 8 * ((lane >> 3) & 1), c = 2 * ks + (lane >> 4);
-        ldsm_x4(s_q + swz(row, c), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
-    }
-
     float o[16][4];
 #pragma unroll
     for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
@@ -223,13 +218,18 @@ __global__ void __launch_bounds__(128) attn3_kernel(const __grid_constant__ Attn
         for (int n = 0; n < 4; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
+            uint32_t qa[4];                                   // Q A-fragment of k-step ks (re-read: registers)
+            {
+                const int row = (lane & 7) + 8 * ((lane >> 3) & 1), c = 2 * ks + (lane >> 4);
+                ldsm_x4(s_q + swz(row, c), qa[0], qa[1], qa[2], qa[3]);
+            }
 #pragma unroll
             for (int np2 = 0; np2 < 2; ++np2) {              // n-tiles 2*np2, 2*np2+1
                 uint32_t b0, b1, b2, b3;
                 const int key = 16 * np2 + 8 * (lane >> 4) + (lane & 7), c = 2 * ks + ((lane >> 3) & 1);
                 ldsm_x4(sk + swz(key, c), b0, b1, b2, b3);
-                mma16816(sacc[2 * np2], qa[ks], b0, b1);
-                mma16816(sacc[2 * np2 + 1], qa[ks], b2, b3);
+                mma16816(sacc[2 * np2], qa, b0, b1);
+                mma16816(sacc[2 * np2 + 1], qa, b2, b3);
             }
         }
         // ---- causal mask + online softmax (rows g and g+8 of this thread)
@@ -389,15 +389,15 @@ int attn3_splits(int B, int H, int max_pages, int num_sms) {
     return s;
 }
 
-template <int NST>
+template <int NST, int MINB>
 static cudaError_t attn3_launch_t(const AttnArgs& a, int splits, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e =
-            cudaFuncSetAttribute(attn3_kernel<NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, A3Cfg<NST>::SMEM);
+            cudaFuncSetAttribute(attn3_kernel<NST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, A3Cfg<NST>::SMEM);
         if (e != cudaSuccess) return e;
         if (!getenv("SV_NO_CARVEOUT")) {
-            e = cudaFuncSetAttribute(attn3_kernel<NST>, cudaFuncAttributePreferredSharedMemoryCarveout,
+            e = cudaFuncSetAttribute(attn3_kernel<NST, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared);
             if (e != cudaSuccess) return e;
         }
@@ -422,7 +422,7 @@ static cudaError_t attn3_launch_t(const AttnArgs& a, int splits, cudaStream_t st
     }
     cfg.attrs = at;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, attn3_kernel<NST>, a);
+    return cudaLaunchKernelEx(&cfg, attn3_kernel<NST, MINB>, a);
 }
 
 // max_ctx_len: the longest cached context of the batch (sizes the per-warp ring)
@@ -433,9 +433,24 @@ cudaError_t attn3_launch(const AttnArgs& a, int splits, int max_ctx_len, cudaStr
     // loads overlap each other's tensor-core work — measured C4 45.8 -> 42.9 ms and
     // C5 8.30 -> 7.88 ms against the 2-stage ring at one CTA (4 warps) per SM
     (void)max_ctx_len;
-    if (g_attn_nst == 2) return attn3_launch_t<2>(a, splits, st);
-    if (g_attn_nst == 3) return attn3_launch_t<3>(a, splits, st);
-    return attn3_launch_t<1>(a, splits, st);
+    if (g_attn_nst == 2) return attn3_launch_t<2, 1>(a, splits, st);
+    if (g_attn_nst == 3) return attn3_launch_t<3, 1>(a, splits, st);
+    // three CTAs per SM when every CTA is resident at once anyway (C2: co-residency with
+    // the GEMM grids) or when the waves stay full (C4: 18.4 of 19 waves), two when the
+    // third CTA per SM would only shorten the grid into a mostly idle tail wave (C5: 512
+    // CTAs = 1.15 waves of 444 vs 1.73 of 296; measured C5 8.62 vs 7.89 ms, C4 42.8 vs
+    // 43.5, C2 3.056 vs 3.072)
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const double ctas = (double)splits * a.B * a.n_heads;
+    auto eff = [&](int k) { const double w = ctas / (k * sms); return w / std::ceil(w); };
+    bool three = ctas <= 2.0 * sms || eff(3) * 1.03 >= eff(2);
+    if (g_attn_minb) three = g_attn_minb == 3;
+    return three ? attn3_launch_t<1, 3>(a, splits, st) : attn3_launch_t<1, 2>(a, splits, st);
 }
 
 }  // namespace sv

@@ -6,7 +6,7 @@ HERE="$(cd "$(dirname "$0")" && pwd)"
 OUT="${1:-$HERE/../libsv.so}"
 shift || true
 NVCC="${NVCC:-/usr/local/cuda/bin/nvcc}"
-OBJ="$HERE/../build"
+OBJ="${SV_OBJ_DIR:-$HERE/../build}"
 LOG="$HERE/../build.log"
 mkdir -p "$OBJ"
 FLAGS=(-std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a

@@ -458,6 +458,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (const char* pf = getenv("SV_PF")) e->pf_depth = atoi(pf);
     if (const char* as = getenv("SV_ATTN_SPLITS")) e->attn_splits = atoi(as);
     if (const char* ns = getenv("SV_ATTN_NST")) g_attn_nst = atoi(ns);
+    if (const char* mb = getenv("SV_A3_MINB")) g_attn_minb = atoi(mb);
     if (getenv("SV_SPLIT_ANY")) g_split_any = true;
     if (getenv("SV_NO_BOX")) e->no_box = true;
     if (getenv("SV_NO_WAVE")) e->no_wave = true;

@@ -108,6 +108,7 @@ cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st);
 // online softmax in registers, cluster (DSMEM) split merge
 int attn3_splits(int B, int H, int max_pages, int num_sms);
 cudaError_t attn3_launch(const AttnArgs& a, int splits, int max_ctx_len, cudaStream_t st);
+extern int g_attn_minb;    // env SV_A3_MINB: 2 or 3 attention CTAs per SM (default: by waves)
 extern int g_attn_nst;     // env SV_ATTN_NST: per-warp ring depth 2 or 3 (default 1)
 
 // ----------------------------------------------------------- acceptance (K5)

@@ -7,6 +7,7 @@ namespace sv {
 
 bool g_use_pdl = true;
 int g_attn_nst = 0;
+int g_attn_minb = 0;
 
 // K4: h^(0) = E[token] (Eq. 3), fp32 residual; u = bf16(h * g_attn[0]);
 // ssq[t][m] = sum of h^2 over the 128-column tile t (RMSNorm statistics for layer 1).
