@@ -1,8 +1,10 @@
 export PYTHONUNBUFFERED=1
-for cfg in "--batch 16 --ctx 2048" "--batch 1 --ctx 512"; do
-SV_KTRACE=gpurun_out/kt.csv timeout 300 python tools/ncu_step.py $cfg --steps 3 > /dev/null 2>&1
-echo "== $cfg"; python tools/ktrace_report.py gpurun_out/kt.csv 2>&1 | head -14
-done
-for cfg in "X=1" "SV_SPLIT_ANY=1"; do env $cfg timeout 600 python bench.py --config C5 --no-cpu-baseline --steps 10 --warmup 3 > gpurun_out/b.json 2>gpurun_out/b.err
-python -c "
-import json; d=json.load(open('gpurun_out/b.json')); r=d['roofline']; print('C5 $cfg', d['latency_p50_ms'])" || tail -3 gpurun_out/b.err; done
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+run() { # tag config env...
+  tag=$1; c=$2; shift 2
+  env "$@" timeout 900 python bench.py --config $c --no-cpu-baseline --steps 10 --warmup 3 > gpurun_out/b.json 2>gpurun_out/b.err
+  python -c "
+import json; d=json.load(open('gpurun_out/b.json')); r=d['roofline']; print('$tag', d['latency_p50_ms'], d['value'], r['step_frac_of_peak'], {k:v['ms'] for k,v in r['kernels'].items() if k in ('gemm_o','gemm_down')})" || tail -3 gpurun_out/b.err
+}
+ALT=SV_LIB=$PWD/paper_2505_21594_b200/libsv_alt.so
+for c in C5 C5 C4 C2; do run "$c stash" $c X=1; run "$c old" $c $ALT; done
