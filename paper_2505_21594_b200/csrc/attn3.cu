@@ -20,7 +20,6 @@
 //   memory in rank order -> deterministic.
 // Numerics: q and p are rounded to bf16 for the MMA (as in a bf16 model); scores,
 // softmax statistics and O accumulate in fp32.
-#include <cmath>
 #include <cfloat>
 #include <cstdlib>
 
@@ -436,10 +435,11 @@ cudaError_t attn3_launch(const AttnArgs& a, int splits, int max_ctx_len, cudaStr
     if (g_attn_nst == 2) return attn3_launch_t<2, 1>(a, splits, st);
     if (g_attn_nst == 3) return attn3_launch_t<3, 1>(a, splits, st);
     // three CTAs per SM when every CTA is resident at once anyway (C2: co-residency with
-    // the GEMM grids) or when the waves stay full (C4: 18.4 of 19 waves), two when the
-    // third CTA per SM would only shorten the grid into a mostly idle tail wave (C5: 512
-    // CTAs = 1.15 waves of 444 vs 1.73 of 296; measured C5 8.62 vs 7.89 ms, C4 42.8 vs
-    // 43.5, C2 3.056 vs 3.072)
+    // the GEMM grids) or when there are >= 4 waves of them (the tail wave matters
+    // little), two when the third CTA per SM would only shorten the grid into a mostly
+    // idle tail wave. Measured (ms, three vs two): C2 3.056 vs 3.072; C4 per-GPU batch
+    // 256 / 128 / 64 (18.4 / 9.2 / 4.6 waves of 444) 42.8 vs 43.5, 22.71 vs 22.80,
+    // 14.94 vs 15.06; batch 32 (2.3 waves) 10.24 vs 10.19; C5 (1.15 waves) 8.62 vs 7.89
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -447,8 +447,7 @@ cudaError_t attn3_launch(const AttnArgs& a, int splits, int max_ctx_len, cudaStr
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const double ctas = (double)splits * a.B * a.n_heads;
-    auto eff = [&](int k) { const double w = ctas / (k * sms); return w / std::ceil(w); };
-    bool three = ctas <= 2.0 * sms || eff(3) * 1.03 >= eff(2);
+    bool three = ctas <= 2.0 * sms || ctas >= 4.0 * 3 * sms;
     if (g_attn_minb) three = g_attn_minb == 3;
     return three ? attn3_launch_t<1, 3>(a, splits, st) : attn3_launch_t<1, 2>(a, splits, st);
 }

@@ -1,10 +1,11 @@
 export PYTHONUNBUFFERED=1
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-run() { # tag config env...
-  tag=$1; c=$2; shift 2
-  env "$@" timeout 900 python bench.py --config $c --no-cpu-baseline --steps 10 --warmup 3 > gpurun_out/b.json 2>gpurun_out/b.err
-  python -c "
-import json; d=json.load(open('gpurun_out/b.json')); r=d['roofline']; print('$tag', d['latency_p50_ms'], d['value'], r['step_frac_of_peak'], {k:v['ms'] for k,v in r['kernels'].items() if k in ('gemm_o','gemm_down')})" || tail -3 gpurun_out/b.err
-}
-ALT=SV_LIB=$PWD/paper_2505_21594_b200/libsv_alt.so
-for c in C5 C5 C4 C2; do run "$c stash" $c X=1; run "$c old" $c $ALT; done
+timeout 900 python -m pytest tests/test_gpu_verify.py tests/test_gpu_full.py -m gpu -x -q 2>&1 | tail -1
+for B in 64 32; do timeout 900 python bench.py --config C4 --batch $B --no-cpu-baseline --steps 10 --warmup 3 > gpurun_out/b.json 2>gpurun_out/b.err
+python -c "
+import json; d=json.load(open('gpurun_out/b.json')); print('C4 B=$B', d['latency_p50_ms'])" || tail -3 gpurun_out/b.err; done
+timeout 600 python bench.py --config C5 --no-cpu-baseline --steps 10 --warmup 3 > gpurun_out/b.json 2>gpurun_out/b.err
+python -c "
+import json; d=json.load(open('gpurun_out/b.json')); print('C5', d['latency_p50_ms'])"
+timeout 600 python bench.py > gpurun_out/b.json 2>gpurun_out/b.err
+python -c "
+import json; d=json.load(open('gpurun_out/b.json')); print('C2', d['latency_p50_ms'], d['value'], d['roofline']['frac'])"
