@@ -403,6 +403,9 @@ def run_ours(args):
                 t.wait_early()
         f = t.wait_final()
         t.release()
+        bad = [r.status for r in f if r.status != sv.SV_OK]
+        if bad:
+            raise RuntimeError(f"verify step returned per-request errors {bad}")
         return sum(r.accepted + 1 for r in f), f
 
     # warm-up (also captures the CUDA graph)
@@ -472,12 +475,8 @@ def run_ours(args):
         f[0] += r["bytes"]
         f[1] += r["ms"]
         f[2] += 1
-    if "fused_step" in fam:     # the whole step is one persistent kernel: it is the dominant kernel
-        dom_kinds, dom_name, tr_key = ["fused_step"], ("fused_step_kernel (persistent: tcgen05 + TMA GEMM "
-                                                       "segments, attention, acceptance)"), "fused"
-    else:
-        dom_kinds = [k for k in fam if k.startswith("gemm")]
-        dom_name, tr_key = "gemm_kernel (QKV/O/gate-up/down/LM-head, tcgen05 + TMA)", "gemm"
+    dom_kinds = [k for k in fam if k.startswith("gemm")]
+    dom_name, tr_key = "gemm_kernel (QKV/O/gate-up/down/LM-head, tcgen05 + TMA)", "gemm"
     g_bytes = sum(fam[k][0] for k in dom_kinds)
     g_ms = sum(fam[k][1] for k in dom_kinds)
     g_n = sum(fam[k][2] for k in dom_kinds)
@@ -527,7 +526,7 @@ def run_ours(args):
                                    + f", stochastic acceptance, alpha {args.alpha}",
                        "global_batch": total, "seq_len": ctx, "gamma": gamma,
                        "exit_layer": exit_layers if exit_layers else exit_layer,
-                       "engine": "fused persistent step kernel" if eng.fused else "per-op kernels + CUDA graph + PDL",
+                       "engine": "per-op kernels + CUDA graph + PDL",
                        "parallelism": f"requests sharded over {world} GPU(s), weights replicated",
                        "l2": "inputs larger than L2 (13.5 GB of weights streamed per step)"},
             "tokens_per_step": round(tot_tokens / (args.steps * total), 4),

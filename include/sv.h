@@ -41,7 +41,7 @@ extern "C" {
 #endif
 
 #define SV_MAX_GAMMA 8
-#define SV_ABI_VERSION 2
+#define SV_ABI_VERSION 3
 
 typedef enum {
     SV_OK = 0,
@@ -64,7 +64,8 @@ SV_API int sv_abi_version(void);
 /* Llama-style decoder shape.  The paper names only "Llama2-7B";
  * constants follow HF Llama-2 (R6).  Constraints: d_model % 128 == 0,
  * head_dim in {32, 64, 128}, n_heads * head_dim == d_model, d_ff % 64 == 0,
- * vocab % 128 == 0, page_tokens == 64, max_ctx % page_tokens == 0. */
+ * vocab % 128 == 0, page_tokens == 64, max_ctx % page_tokens == 0, max_ctx <= 4096
+ * (an attention CTA stages at most 64 pages of its page list). */
 typedef struct {
     int32_t n_layers, d_model, n_heads, head_dim, d_ff, vocab, max_ctx, page_tokens;
     float rms_eps;      /* 1e-5  */
@@ -137,9 +138,6 @@ typedef struct {
     int32_t max_batch;   /* max requests per submit (>= 1)                          */
     int32_t max_gamma;   /* max draft length per submit (1..SV_MAX_GAMMA)           */
     int32_t use_graphs;  /* 1: replay one CUDA graph per (batch, gamma, exit, ctx)  */
-    int32_t fused;       /* 1: the whole step is ONE persistent kernel (one CTA per
-                            SM, stream-K GEMM segments, device-side dependency
-                            counters); 0: one kernel per op       */
     int32_t max_prefill; /* max prompt tokens of one sv_prefill (0 = no prefill;
                             sizes the activation buffers: rows = max(max_batch *
                             (max_gamma + 1), max_prefill))                      */
@@ -218,7 +216,7 @@ SV_API sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us);   /* KV alread
  * 31 exits for Llama2-7B).
  * exit_layers: host [n_exits], strictly ascending, each in 1..n_layers (n_layers
  * itself = an exit at the final layer, bitwise equal to the final result);
- * n_exits <= n_layers <= 64; the fused engine accepts n_exits <= 1.  Every exit
+ * n_exits <= n_layers <= 64.  Every exit
  * uses the same Philox counters as the final exit (R10) and none of
  * them changes the session (KV, length).
  * early: host [n_exits][n]; row k is valid after sv_wait_exit(t, k) (or after
@@ -242,7 +240,7 @@ SV_API sv_status sv_ticket_release(sv_ticket* t);
  * argmax (sample = 0) or a sample of p (sample = 1; the session's Philox stream at
  * round_id = last_round + 1, which the call consumes).  out->tokens[0] = next
  * token (the pending token of the first verify round), out->new_len = len + n.
- * Synchronous; n <= opts.max_prefill (SV_E_CAPACITY), per-op engine only. */
+ * Synchronous; n <= opts.max_prefill (SV_E_CAPACITY). */
 SV_API sv_status sv_prefill(sv_session* s, const int32_t* tokens, int32_t n, int32_t sample, sv_exit_result* out);
 
 /* The north star's synchronous form: verify(draft_tokens, draft_probs, kv) ->
@@ -269,8 +267,7 @@ SV_API sv_status sv_debug_kv_rows(sv_session* s, int32_t layer, int32_t first, i
  * bytes / flops = algorithmic work of the launch. */
 enum {
     SV_K_EMBED = 0, SV_K_QKV = 1, SV_K_ATTN = 2, SV_K_O = 3, SV_K_GU = 4, SV_K_DOWN = 5,
-    SV_K_LM_EXIT = 6, SV_K_ACCEPT_EXIT = 7, SV_K_LM_FINAL = 8, SV_K_ACCEPT_FINAL = 9,
-    SV_K_FUSED = 10   /* the whole step as one persistent kernel (opts.fused) */
+    SV_K_LM_EXIT = 6, SV_K_ACCEPT_EXIT = 7, SV_K_LM_FINAL = 8, SV_K_ACCEPT_FINAL = 9
 };
 typedef struct {
     int32_t kind;    /* SV_K_*                                   */

@@ -125,12 +125,25 @@ def accept_greedy(z: np.ndarray, drafts) -> Result:
                   float(probs[delta][nxt]), OK, margins)
 
 
+def philox_uniforms(seed: int, session_id: int, round_id: int):
+    """The session's counter-based uniforms: a function
+    (row, purpose, n) -> n uniforms of (purpose, logits row, round, session)."""
+    return lambda row, purpose, n: philox.uniforms(seed, session_id, round_id, row, purpose, n)
+
+
 def accept_stochastic(z: np.ndarray, drafts, q: np.ndarray, seed: int, session_id: int,
-                      round_id: int) -> Result:
+                      round_id: int, uniforms=None, sample=None) -> Result:
     """z [G, V] target logits; drafts [gamma]; q [gamma, V] draft distributions
-    (q[j-1] is q_j, the distribution x_j was drafted from)."""
+    (q[j-1] is q_j, the distribution x_j was drafted from).
+
+    uniforms(row, purpose, n) supplies the random numbers (default: the session's
+    Philox stream); sample(w, u) -> (token, margin) draws from normalize(w)
+    (default: the exponential race).  Both are parameters so the tests can
+    enumerate the rule's branches exactly (tests/test_oracle_accept.py)."""
     z = np.asarray(z, dtype=np.float64)
     q = np.asarray(q, dtype=np.float64)
+    uniforms = uniforms or philox_uniforms(seed, session_id, round_id)
+    sample = sample or race
     gamma = len(drafts)
     V = z.shape[1]
     # a drafted token the drafter gave no mass is a corrupt batch (SPEC.md:129),
@@ -143,19 +156,19 @@ def accept_stochastic(z: np.ndarray, drafts, q: np.ndarray, seed: int, session_i
     for j in range(1, gamma + 1):
         x = int(drafts[j - 1])
         ratio = p[j - 1][x] / q[j - 1, x]
-        u = philox.uniforms(seed, session_id, round_id, j - 1, philox.PURPOSE_ACCEPT, 1)[0]
+        u = uniforms(j - 1, philox.PURPOSE_ACCEPT, 1)[0]
         margins.append(("ratio", j - 1, abs(u - ratio)))
         if not (u < ratio):
             break
         delta = j
-    if delta < gamma:
-        w = np.maximum(0.0, p[delta] - q[delta])        # q_{delta+1} is q[delta]
-        if not w.sum() > 0.0:
+    if delta < gamma:                                   # rejection at x_{delta+1}, q_{delta+1} = q[delta]
+        try:
+            w = residual_distribution(p[delta], q[delta])
+        except ValueError:                              # numerically all-zero residual (R13)
             w = p[delta]
-    else:
+    else:                                               # all accepted: bonus token from p_gamma
         w = p[gamma]
-    uv = philox.uniforms(seed, session_id, round_id, delta, philox.PURPOSE_RACE, V)
-    nxt, m = race(w, uv)
+    nxt, m = sample(w, uniforms(delta, philox.PURPOSE_RACE, V))
     margins.append(("race", delta, m))
     score = max(confidence(p[r]) for r in range(delta + 1))
     return Result(delta, [int(t) for t in drafts[:delta]] + [nxt], score,

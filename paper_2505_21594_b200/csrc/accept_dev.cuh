@@ -1,6 +1,6 @@
 // accept_dev.cuh — device bodies of K5/K6 (vocabulary statistics, Leviathan
 // acceptance, residual / bonus race, rollback length), shared by the per-op
-// kernels (accept.cu) and the fused step kernel (step.cu).
+// kernels (accept.cu).
 //
 // Letters: p = target (softmax of the logits), q = draft distribution.
 // Rule (R2, Eq. 2, adopted from Leviathan):

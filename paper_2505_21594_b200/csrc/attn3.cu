@@ -426,26 +426,26 @@ static cudaError_t attn3_launch_t(const AttnArgs& a, int splits, cudaStream_t st
 
 // max_ctx_len: the longest cached context of the batch (sizes the per-warp ring)
 cudaError_t attn3_launch(const AttnArgs& a, int splits, int max_ctx_len, cudaStream_t st) {
-    if (a.head_dim != A3_D || a.page_tokens != 64 || a.G > 16 || splits < 1 || splits > 8)
+    if (a.head_dim != A3_D || a.page_tokens != 64 || a.G > 16 || splits < 1 || splits > 8 || a.num_sms < 1)
         return cudaErrorInvalidValue;
+    // a CTA stages its page list in sBlk[64]: at most 64 pages per split
+    const int max_pages = (max_ctx_len + a.G + 63) / 64;
+    if ((max_pages + splits - 1) / splits > 64) return cudaErrorInvalidValue;
     // 1-stage ring at every context length: 69 KB, two CTAs (8 warps) per SM, whose
     // loads overlap each other's tensor-core work — measured C4 45.8 -> 42.9 ms and
     // C5 8.30 -> 7.88 ms against the 2-stage ring at one CTA (4 warps) per SM
-    (void)max_ctx_len;
     if (g_attn_nst == 2) return attn3_launch_t<2, 1>(a, splits, st);
     if (g_attn_nst == 3) return attn3_launch_t<3, 1>(a, splits, st);
-    // three CTAs per SM when every CTA is resident at once anyway (C2: co-residency with
-    // the GEMM grids) or when there are >= 4 waves of them (the tail wave matters
-    // little), two when the third CTA per SM would only shorten the grid into a mostly
-    // idle tail wave. Measured (ms, three vs two): C2 3.056 vs 3.072; C4 per-GPU batch
-    // 256 / 128 / 64 (18.4 / 9.2 / 4.6 waves of 444) 42.8 vs 43.5, 22.71 vs 22.80,
-    // 14.94 vs 15.06; batch 32 (2.3 waves) 10.24 vs 10.19; C5 (1.15 waves) 8.62 vs 7.89
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    // registers for three CTAs per SM when the whole grid is resident at two per SM
+    // anyway (ctas <= 2 x SMs: the lower register budget leaves room for the
+    // neighbouring GEMM grids' CTAs under PDL) or when there are >= 4 waves of
+    // three (the tail wave matters little); two otherwise.  Measured (ms, three vs
+    // two): C2 (256 CTAs) 3.056 vs 3.072; C4 per-GPU batch 256 / 128 / 64 (18.4 /
+    // 9.2 / 4.6 waves of 444) 42.8 vs 43.5, 22.71 vs 22.80, 14.94 vs 15.06; batch 32
+    // (2.3 waves) 10.24 vs 10.19; C5 (512 CTAs, 1.15 waves of 444) 8.62 vs 7.89.
+    // The band 2 x SMs < ctas <= 3 x SMs (one resident wave at three) is unmeasured
+    // and keeps two.
+    const int sms = a.num_sms;
     const double ctas = (double)splits * a.B * a.n_heads;
     bool three = ctas <= 2.0 * sms || ctas >= 4.0 * 3 * sms;
     if (g_attn_minb) three = g_attn_minb == 3;

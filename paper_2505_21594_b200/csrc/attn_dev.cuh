@@ -1,6 +1,6 @@
 // attn_dev.cuh — device body of K3 (gamma-query causal attention over one
 // 64-key page of the paged bf16 KV cache, plus the in-order page merge by the
-// last finisher), shared by attn.cu and the fused step kernel.
+// last finisher), used by attn.cu (head_dim != 128).
 //
 //   a_j = softmax(q_j K^T / sqrt(Dh)) V   over keys 0 .. ctx_b + j      (Eq. 3)
 #pragma once

@@ -12,7 +12,7 @@ mkdir -p "$OBJ"
 FLAGS=(-std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a
        -Xcompiler -fPIC -Xcompiler -fvisibility=hidden
        -Xptxas -v --expt-relaxed-constexpr "$@")
-SRCS=(engine gemm attn accept misc fused attn3 gemm_big)
+SRCS=(engine gemm attn accept misc attn3 gemm_big)
 : > "$LOG"
 pids=()
 for s in "${SRCS[@]}"; do

@@ -26,7 +26,6 @@
 #include <vector>
 
 #include "../../include/sv.h"
-#include "fused.h"
 #include "kernels.h"
 
 using namespace sv;
@@ -68,7 +67,7 @@ static sv_status check_cfg(const sv_model_cfg* c) {
     if (c->n_layers < 1 || c->d_model <= 0 || c->d_model % 128 || c->n_heads <= 0 ||
         c->n_heads * c->head_dim != c->d_model || !(c->head_dim == 32 || c->head_dim == 64 || c->head_dim == 128) ||
         c->d_ff <= 0 || c->d_ff % 64 || c->vocab <= 0 || c->vocab % 128 || c->page_tokens != 64 ||
-        c->max_ctx <= 0 || c->max_ctx % c->page_tokens)
+        c->max_ctx <= 0 || c->max_ctx % c->page_tokens || c->max_ctx > 4096)
         return fail(SV_E_INVALID, "unsupported model shape (see sv_model_cfg constraints)");
     return SV_OK;
 }
@@ -203,7 +202,7 @@ struct sv_ticket {
     int nb = 0, gamma = 0;
     bool has_gpu;
     bool final_done = false;
-    cudaEvent_t ev_done;
+    cudaEvent_t ev_done = nullptr;
 };
 
 struct sv_engine {
@@ -257,10 +256,8 @@ struct sv_engine {
     volatile uint64_t* mb_flag;
     sv_exit_result* mb_exit_dev = nullptr;      // device aliases of the mapped mailboxes
     uint64_t* mb_flag_dev = nullptr;
-    // fused persistent step: device-resident tensor maps and per-key plans
-    CUtensorMap* d_tmaps = nullptr;             // [4L+1 weights][5 tile sizes x 4 activation maps]
-    std::map<StepKey, FusedPlan*> plans;
-    FusedPlan* last_plan = nullptr;
+    // device-resident weight tensor maps (L2 prefetch of the next GEMM, env SV_PF)
+    CUtensorMap* d_tmaps = nullptr;             // [qkv L][o L][gu L][down L][lm]
     // tensor maps
     std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;
     CUtensorMap tm_lm;
@@ -318,7 +315,7 @@ static sv_status engine_alloc(sv_engine* e) {
     CK(dalloc((void**)&e->cnt_exit, (size_t)max_tiles * 4));
     // attention partials
     e->max_nchunk = e->cfg.max_ctx / 64 + 1;
-    // per-page attention partials (attn_kernel, head_dim != 128, and the fused kernel)
+    // per-page attention partials (attn_kernel, head_dim != 128)
     const size_t bh = (size_t)(e->D == 128 ? e->opts.max_batch : e->max_vreq) * e->H;
     const int G = std::max(e->opts.max_gamma + 1, 8);
     CK(dalloc((void**)&e->attn_o, bh * e->max_nchunk * G * e->D * 4));
@@ -334,6 +331,9 @@ static sv_status engine_alloc(sv_engine* e) {
     CK(dalloc((void**)&e->cnt_acc_final, (size_t)e->opts.max_batch * 4));
     CK(dalloc((void**)&e->res_exit_dev, (size_t)e->opts.max_batch * sizeof(sv_exit_result)));
     CK(dalloc((void**)&e->res_final_dev, (size_t)e->opts.max_batch * sizeof(sv_exit_result)));
+    // device staging of host draft probabilities (allocated up front: a submit must
+    // not fail half-way through marking its sessions busy)
+    CK(dalloc((void**)&e->probs_stage, (size_t)e->opts.max_batch * e->opts.max_gamma * V * 4));
     // RoPE table (cos, sin) in double -> fp32: angle = pos * theta^(-2i/Dh)
     {
         const int half = e->D / 2, npos = e->cfg.max_ctx + 16;
@@ -405,11 +405,9 @@ static sv_status engine_tmaps(sv_engine* e) {
         if (!act_maps(e, tn, &m)) return fail(SV_E_DEVICE, "tensor map (activations)");
         e->tm_act[tn] = m;
     }
-    // device copy for the fused kernel: weights [qkv L][o L][gu L][down L][lm], then
-    // activation maps at 4L+1 + 4*ti + k (ti = index of the tile size, k = buffer)
-    const int L = e->L, nmaps = 4 * L + 1 + 20;
+    // device copy of the weight maps [qkv L][o L][gu L][down L][lm] (L2 prefetch, SV_PF)
+    const int L = e->L, nmaps = 4 * L + 1;
     std::vector<CUtensorMap> all(nmaps);
-    memset(all.data(), 0, sizeof(CUtensorMap) * nmaps);
     for (int l = 0; l < L; ++l) {
         all[l] = e->tm_qkv[l];
         all[L + l] = e->tm_o[l];
@@ -417,27 +415,10 @@ static sv_status engine_tmaps(sv_engine* e) {
         all[3 * L + l] = e->tm_down[l];
     }
     all[4 * L] = e->tm_lm;
-    int ti = 0;
-    for (int tn : {16, 32, 64, 128, 256}) {
-        auto it = e->tm_act.find(tn);
-        if (it != e->tm_act.end())
-            for (int k = 0; k < 4; ++k) all[4 * L + 1 + 4 * ti + k] = it->second[k];
-        ++ti;
-    }
     CK(cudaMalloc((void**)&e->d_tmaps, sizeof(CUtensorMap) * nmaps));
     CK(cudaMemcpy(e->d_tmaps, all.data(), sizeof(CUtensorMap) * nmaps, cudaMemcpyHostToDevice));
-    // weight maps in [qkv L][o L][gu L][down L][lm] order
-    e->wmap128.assign(all.begin(), all.begin() + 4 * L + 1);
+    e->wmap128 = all;
     return SV_OK;
-}
-
-static const CUtensorMap* dev_act_map(sv_engine* e, int tn, int k) {
-    int ti = 0;
-    for (int t : {16, 32, 64, 128, 256}) {
-        if (t == tn) break;
-        ++ti;
-    }
-    return e->d_tmaps + 4 * e->L + 1 + 4 * ti + k;
 }
 
 extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights* w, const sv_engine_opts* opts,
@@ -498,7 +479,6 @@ extern "C" sv_status sv_engine_set_adapters(sv_engine* e, const sv_adapters* ad)
     if (!e) return fail(SV_E_INVALID, "NULL engine");
     std::lock_guard<std::mutex> lk(e->mu);
     if (e->inflight) return fail(SV_E_BUSY, "a ticket is in flight");
-    if (ad && e->opts.fused) return fail(SV_E_INVALID, "exit adapters run on the per-op engine");
     CK(cudaSetDevice(e->device));
     const int L = e->L, d = e->d;
     if (ad) {
@@ -541,10 +521,6 @@ extern "C" sv_status sv_engine_destroy(sv_engine* e) {
     cudaSetDevice(e->device);
     cudaDeviceSynchronize();
     for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
-    for (auto& kv : e->plans) {
-        fused_free(kv.second);
-        delete kv.second;
-    }
     if (e->d_tmaps) cudaFree(e->d_tmaps);
     void* dev[] = {e->h, e->qbuf, e->ssq, e->logits_exit, e->logits_final, e->ws_main, e->ws_exit, e->rope,
                    e->attn_o, e->attn_ml, e->u, e->u_exit, e->attn_out, e->act, e->cnt_main, e->cnt_exit,
@@ -652,21 +628,11 @@ static float* ssq_at(sv_engine* e, int layer, int which) {   // norm point (laye
     return e->ssq + (size_t)(2 * layer + which) * (e->d / 128) * e->MP;
 }
 
-static cudaError_t issue_fused(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk,
-                               int* launches);
-
-static int mask_single_exit(uint64_t mask) {   // the exit layer of a one-exit mask, 0 if none
-    for (int l = 1; l <= 64; ++l)
-        if (mask & (1ull << (l - 1))) return l;
-    return 0;
-}
-
 // Issues every kernel / copy of one step on (main, exit) streams; returns launch count.
 // exit_mask: bit l-1 = early exit after decoder layer l; the k-th exit (ascending)
 // uses u_exit slot k, mailbox rows [k][B] and flag k (streamed as each completes).
 static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, uint64_t exit_mask, int nchunk,
                               int* launches) {
-    if (e->opts.fused) return issue_fused(e, st, n, gamma, mask_single_exit(exit_mask), nchunk, launches);
     const bool pf = e->pf.on;                 // prefill: one session's prompt as query blocks
     const int G = gamma + 1, M = pf ? e->pf.n_tokens : n * G, d = e->d, F = e->F, V = e->V, L = e->L;
     const int nA = pf ? e->pf.nq : n, GA = pf ? e->pf.gb : G;   // attention "requests" and their rows
@@ -836,6 +802,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
                 aa.ctx_pre = (const int32_t*)(e->meta_dev + e->off_cpre);
             }
             aa.layer = l; aa.page_tokens = e->cfg.page_tokens; aa.nchunk = nchunk;
+            aa.num_sms = e->num_sms;
             aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)e->D));
             aa.ktrace = e->ktrace;
             aa.ktrace_id = nl;
@@ -921,195 +888,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
     return cudaSuccess;
 }
 
-// ------------------------------------------------------------ fused step plan
-// Same ops, same epilogue arguments as issue_step, expressed as stages of the
-// persistent kernel (fused.cu).  Also returns the step's algorithmic bytes /
-// flops (the same per-op formulas as the per-op profile).
-static cudaError_t build_fused_plan(sv_engine* e, int n, int gamma, int exit_layer, int nchunk, FusedPlan* P,
-                                    double* bytes, double* flops) {
-    const int G = gamma + 1, M = n * G, d = e->d, F = e->F, V = e->V, L = e->L;
-    const int tn = gemm_pick_tile_n(M), MT = (M + tn - 1) / tn;
-    const double Md = (double)M * d;
-    double B = 0, FL = 0;
-    std::vector<FStage> st;
-    auto add = [&](const FStage& s) {
-        st.push_back(s);
-        return (int)st.size() - 1;
-    };
-    auto gemm_stage = [&](int epi, const CUtensorMap* A, const CUtensorMap* Bm, int N, int K, const GemmArgs& g,
-                          int dep, double out_bytes) {
-        FStage s;
-        memset(&s, 0, sizeof(s));
-        s.type = IT_GEMM;
-        s.dep = dep;
-        s.epi = epi;
-        s.nt_n = N / 128;
-        s.nt_m = MT;
-        s.kblocks = K / 64;
-        s.tmA = A;
-        s.tmB = Bm;
-        s.g = g;
-        s.g.N = N;
-        s.g.K = K;
-        s.g.splits = 1;
-        B += (double)N * K * 2 + (double)M * K * 2 + out_bytes;
-        FL += 2.0 * M * N * K;
-        return s;
-    };
-    auto accept_stage = [&](bool is_exit, int dep, bool stats) {
-        FStage s;
-        memset(&s, 0, sizeof(s));
-        s.type = stats ? IT_STATS : IT_ACCEPT;
-        s.dep = dep;
-        s.is_exit = is_exit ? 1 : 0;
-        AcceptArgs& aa = s.ac;
-        aa.logits = is_exit ? e->logits_exit : e->logits_final;
-        aa.req = (const ReqDev*)(e->meta_dev + e->off_reqdev);
-        aa.stats = is_exit ? e->stats_exit : e->stats_final;
-        aa.race = is_exit ? e->race_exit : e->race_final;
-        aa.counters = is_exit ? e->cnt_acc_exit : e->cnt_acc_final;
-        aa.out = is_exit ? e->res_exit_dev : e->res_final_dev;
-        aa.B = n; aa.G = G; aa.V = V; aa.nch = e->acc_nch; aa.chunk = e->acc_chunk;
-        aa.exit_layer = is_exit ? exit_layer : L;
-        aa.is_final = is_exit ? 0 : 1;
-        B += stats ? (double)M * V * 4 : (double)n * V * 8;
-        return s;
-    };
-    const CUtensorMap* tu = dev_act_map(e, tn, 0);
-    const CUtensorMap* ta = dev_act_map(e, tn, 1);
-    const CUtensorMap* tact = dev_act_map(e, tn, 2);
-    const CUtensorMap* tex = dev_act_map(e, tn, 3);
-    FStage emb;
-    memset(&emb, 0, sizeof(emb));
-    emb.type = IT_EMBED;
-    emb.dep = -1;
-    emb.em = EmbedArgs{(const int32_t*)(e->meta_dev + e->off_tok), e->embed, e->norm_attn[0], e->h, e->u,
-                       ssq_at(e, 0, 0), M, e->MP, d};
-    B += Md * 8;
-    int prev = add(emb);
-    const int32_t* ctxh = (const int32_t*)(e->meta_host + e->off_ctx);
-    for (int l = 0; l < L; ++l) {
-        GemmArgs a = base_args(e, M);
-        a.layer = l;
-        a.ssq_in = ssq_at(e, l, 0);
-        a.qbuf = e->qbuf;
-        const int s_qkv = add(gemm_stage(EPI_QKV, e->d_tmaps + l, tu, 3 * d, d, a, prev, Md * 8));
-        FStage at;
-        memset(&at, 0, sizeof(at));
-        at.type = IT_ATTN;
-        at.dep = s_qkv;
-        AttnArgs& aa = at.at;
-        aa.q = e->qbuf; aa.kv_pool = (const bf16_raw_t*)e->kv_pool; aa.out = e->attn_out;
-        aa.part_o = e->attn_o; aa.part_ml = e->attn_ml; aa.counters = e->cnt_attn;
-        aa.ctx = (const int32_t*)(e->meta_dev + e->off_ctx);
-        aa.page_table = (const int32_t*)(e->meta_dev + e->off_pt);
-        aa.pt_stride = e->pt_stride;
-        aa.B = n; aa.G = G; aa.n_heads = e->H; aa.head_dim = e->D; aa.d_model = d; aa.n_layers = L;
-        aa.layer = l; aa.page_tokens = e->cfg.page_tokens; aa.nchunk = nchunk;
-        aa.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)e->D));
-        B += Md * 6;
-        for (int b = 0; b < n; ++b) {
-            B += (double)(ctxh[b] + G) * d * 4;
-            for (int j = 0; j < G; ++j) FL += 4.0 * (ctxh[b] + j + 1) * d;
-        }
-        const int s_at = add(at);
-        GemmArgs o = base_args(e, M);
-        o.h = e->h; o.g_out = e->norm_mlp[l]; o.u_out = e->u; o.ssq_out = ssq_at(e, l, 1);
-        const int s_o = add(gemm_stage(EPI_RESID, e->d_tmaps + L + l, ta, d, d, o, s_at, Md * 10));
-        GemmArgs gu = base_args(e, M);
-        gu.ssq_in = ssq_at(e, l, 1);
-        gu.act = e->act;
-        const int s_gu = add(gemm_stage(EPI_SWIGLU, e->d_tmaps + 2 * L + l, tu, 2 * F, d, gu, s_o, (double)M * F * 2));
-        GemmArgs dn = base_args(e, M);
-        dn.h = e->h;
-        dn.g_out = (l + 1 < L) ? e->norm_attn[l + 1] : e->norm_final;
-        dn.u_out = e->u;
-        if (l + 1 == exit_layer) {
-            dn.g_out2 = e->norm_final;
-            dn.u_out2 = e->u_exit;
-        }
-        dn.ssq_out = ssq_at(e, l + 1, 0);
-        prev = add(gemm_stage(EPI_RESID, e->d_tmaps + 3 * L + l, tact, d, F, dn, s_gu,
-                              Md * (l + 1 == exit_layer ? 12 : 10)));
-        if (l + 1 == exit_layer) {   // S10-S11 on the exit branch, right after h^(l_e) exists
-            GemmArgs lm = base_args(e, M);
-            lm.ssq_in = ssq_at(e, exit_layer, 0);
-            lm.logits = e->logits_exit;
-            FStage s = gemm_stage(EPI_LOGITS, e->d_tmaps + 4 * L, tex, V, d, lm, prev, (double)M * V * 4);
-            s.exit_ws = 1;
-            const int s_lm = add(s);
-            const int s_stats = add(accept_stage(true, s_lm, true));
-            add(accept_stage(true, s_stats, false));
-        }
-    }
-    GemmArgs lm = base_args(e, M);
-    lm.ssq_in = ssq_at(e, L, 0);
-    lm.logits = e->logits_final;
-    const int s_lm = add(gemm_stage(EPI_LOGITS, e->d_tmaps + 4 * L, tu, V, d, lm, prev, (double)M * V * 4));
-    const int s_stats = add(accept_stage(false, s_lm, true));
-    add(accept_stage(false, s_stats, false));
-    const char* cps = getenv("SV_FUSED_CPS");   // CTAs per SM of the persistent grid (library built to fit)
-    cudaError_t r = fused_build(P, st, e->num_sms * (cps ? atoi(cps) : 1), tn, e->D);
-    if (r != cudaSuccess) return r;
-    P->early_host_dev = e->mb_exit_dev;
-    P->early_flag_dev = e->mb_flag_dev;
-    P->seq_dev = (const uint64_t*)(e->meta_dev + e->off_seq);
-    P->n_req = n;
-    *bytes = B;
-    *flops = FL;
-    return cudaSuccess;
-}
-
-static std::map<const FusedPlan*, std::pair<double, double>> g_plan_cost;
-
-// Builds (once per key, outside any stream capture: it allocates and uploads).
-static cudaError_t ensure_plan(sv_engine* e, int n, int gamma, int exit_layer, int nchunk, FusedPlan** out) {
-    StepKey key{n, gamma, exit_layer > 0 ? 1ull << (exit_layer - 1) : 0ull, nchunk};
-    auto it = e->plans.find(key);
-    if (it != e->plans.end()) {
-        *out = it->second;
-        return cudaSuccess;
-    }
-    FusedPlan* P = new FusedPlan();
-    double b = 0, f = 0;
-    cudaError_t r = build_fused_plan(e, n, gamma, exit_layer, nchunk, P, &b, &f);
-    if (r != cudaSuccess) {
-        fused_free(P);
-        delete P;
-        return r;
-    }
-    g_plan_cost[P] = {b, f};
-    e->plans[key] = P;
-    *out = P;
-    return cudaSuccess;
-}
-
-static cudaError_t issue_fused(sv_engine* e, cudaStream_t st, int n, int gamma, int exit_layer, int nchunk,
-                               int* launches) {
-    FusedPlan* P = nullptr;
-    cudaError_t r0 = ensure_plan(e, n, gamma, exit_layer, nchunk, &P);
-    if (r0 != cudaSuccess) return r0;
-    e->last_plan = P;
-    auto& cost = g_plan_cost;
-    cudaEvent_t a = nullptr, b = nullptr;
-    if (e->prof) {
-        cudaEventCreate(&a);
-        cudaEventRecord(a, st);
-    }
-    cudaError_t r = fused_launch(P, st);
-    if (r != cudaSuccess) return r;
-    if (e->prof) {
-        cudaEventCreate(&b);
-        cudaEventRecord(b, st);
-        e->prof->push_back(ProfRec{SV_K_FUSED, -1, st, a, b, cost[P].first, cost[P].second});
-    }
-    r = cudaMemcpyAsync(e->mb_final, e->res_final_dev, (size_t)n * sizeof(sv_exit_result), cudaMemcpyDeviceToHost, st);
-    *launches = 1;
-    return r;
-}
-
 static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, uint64_t exit_mask, int nchunk) {
-    const int exit_layer = mask_single_exit(exit_mask);   // fused engine: one exit
     CK(cudaMemcpyAsync(e->meta_dev, e->meta_host, e->meta_bytes, cudaMemcpyHostToDevice, st));
     int nl = 0;
     if (!e->opts.use_graphs || e->prof) {
@@ -1120,10 +899,6 @@ static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, uint6
     StepKey key{n, gamma, exit_mask, nchunk};
     auto it = e->graphs.find(key);
     if (it == e->graphs.end()) {
-        if (e->opts.fused) {
-            FusedPlan* P = nullptr;
-            CK(ensure_plan(e, n, gamma, exit_layer, nchunk, &P));
-        }
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(e->s_cap, cudaStreamCaptureModeThreadLocal));
         cudaError_t r = issue_step(e, e->s_cap, n, gamma, exit_mask, nchunk, &nl);
@@ -1151,8 +926,6 @@ extern "C" sv_status sv_verify_submit_exits(sv_engine* e, const sv_verify_req* r
     if (n_exits < 0 || n_exits > e->L || (n_exits > 0 && !exit_layers))
         return fail(SV_E_INVALID, "bad exit layer list");
     if (n_exits > 0 && !early) return fail(SV_E_INVALID, "early result array required when exits are requested");
-    if (n_exits > 1 && e->opts.fused) return fail(SV_E_INVALID, "the fused engine supports one early exit");
-    if (reqs[0].gamma == 0 && e->opts.fused) return fail(SV_E_INVALID, "the fused engine needs gamma >= 1");
     if (n_exits > 0 && e->L > 64) return fail(SV_E_INVALID, "early exits need n_layers <= 64");
     uint64_t exit_mask = 0;
     for (int k = 0; k < n_exits; ++k) {
@@ -1183,6 +956,15 @@ extern "C" sv_status sv_verify_submit_exits(sv_engine* e, const sv_verify_req* r
     t->exit_done.assign(n_exits, false);
     t->gpu_slot.assign(n, -1);
     t->host_status.assign(n, SV_OK);
+    // a CUDA failure after sessions were taken: release them and the ticket, poison
+    auto abort_submit = [&](const std::string& msg) -> sv_status {
+        e->poisoned = true;
+        for (size_t i = 0; i < t->sess.size(); ++i)
+            if (t->gpu_slot[i] >= 0) t->sess[i]->busy = false;
+        if (t->ev_done) cudaEventDestroy(t->ev_done);
+        delete t;
+        return fail(SV_E_DEVICE, msg);
+    };
     // S0: validate protocol state, build the batch of valid requests
     int nb = 0, max_len = 0;
     uint8_t* mh = e->meta_host;
@@ -1224,10 +1006,10 @@ extern "C" sv_status sv_verify_submit_exits(sv_engine* e, const sv_verify_req* r
         for (int j = 0; j < gamma; ++j) r.drafts[j] = q.draft_tokens[j];
         if (q.draft_probs) {
             if (q.probs_on_host) {
-                if (!e->probs_stage)
-                    CK(cudaMalloc(&e->probs_stage, (size_t)e->opts.max_batch * e->opts.max_gamma * e->V * 4));
                 float* dst = e->probs_stage + (size_t)b * e->opts.max_gamma * e->V;
-                CK(cudaMemcpyAsync(dst, q.draft_probs, (size_t)gamma * e->V * 4, cudaMemcpyHostToDevice, st));
+                const cudaError_t ce =
+                    cudaMemcpyAsync(dst, q.draft_probs, (size_t)gamma * e->V * 4, cudaMemcpyHostToDevice, st);
+                if (ce != cudaSuccess) return abort_submit(std::string("draft probs H2D: ") + cudaGetErrorString(ce));
                 r.probs = (uint64_t)dst;
             } else {
                 r.probs = (uint64_t)q.draft_probs;
@@ -1241,19 +1023,22 @@ extern "C" sv_status sv_verify_submit_exits(sv_engine* e, const sv_verify_req* r
     t->seq = ++e->seq;
     *(uint64_t*)(mh + e->off_seq) = t->seq;
     t->has_gpu = nb > 0;
-    CK(cudaEventCreateWithFlags(&t->ev_done, cudaEventDisableTiming));
+    {
+        const cudaError_t ce = cudaEventCreateWithFlags(&t->ev_done, cudaEventDisableTiming);
+        if (ce != cudaSuccess) {
+            t->ev_done = nullptr;
+            return abort_submit(std::string("cudaEventCreate: ") + cudaGetErrorString(ce));
+        }
+    }
     if (t->has_gpu) {
         int nchunk = (max_len + 63) / 64;
         nchunk = std::min(e->max_nchunk, nchunk);   // exact: no empty attention work items
-        sv_status s = run_step(e, st, nb, gamma, exit_mask, nchunk);
-        if (s) {
-            e->poisoned = true;
-            for (auto* ss : t->sess) ss->busy = false;
-            delete t;
-            return s;
-        }
+        if (run_step(e, st, nb, gamma, exit_mask, nchunk)) return abort_submit(g_err);
     }
-    CK(cudaEventRecord(t->ev_done, st));
+    {
+        const cudaError_t ce = cudaEventRecord(t->ev_done, st);
+        if (ce != cudaSuccess) return abort_submit(std::string("cudaEventRecord: ") + cudaGetErrorString(ce));
+    }
     e->inflight = t;
     *out = t;
     return SV_OK;
@@ -1283,7 +1068,12 @@ extern "C" sv_status sv_wait_exit(sv_ticket* t, int32_t k, int64_t timeout_us) {
     if (t->has_gpu) {
         const auto t0 = std::chrono::steady_clock::now();
         while (e->mb_flag[k] != t->seq) {
-            if (cudaEventQuery(t->ev_done) == cudaSuccess) break;   // step already complete
+            const cudaError_t q = cudaEventQuery(t->ev_done);
+            if (q == cudaSuccess) break;   // step already complete
+            if (q != cudaErrorNotReady) {   // a kernel fault: the flag will never arrive
+                e->poisoned = true;
+                return fail(SV_E_DEVICE, std::string("step failed: ") + cudaGetErrorString(q));
+            }
             if (timeout_us >= 0 &&
                 std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count() >
                     timeout_us)
@@ -1305,7 +1095,12 @@ extern "C" sv_status sv_exits_ready(sv_ticket* t, int32_t* n_ready) {
     if (!t || !n_ready) return fail(SV_E_INVALID, "NULL argument");
     sv_engine* e = t->e;
     int k = 0;
-    const bool all = !t->has_gpu || cudaEventQuery(t->ev_done) == cudaSuccess;
+    const cudaError_t q = t->has_gpu ? cudaEventQuery(t->ev_done) : cudaSuccess;
+    if (q != cudaSuccess && q != cudaErrorNotReady) {
+        e->poisoned = true;
+        return fail(SV_E_DEVICE, std::string("step failed: ") + cudaGetErrorString(q));
+    }
+    const bool all = q == cudaSuccess;
     while (k < (int)t->exits.size() && (all || e->mb_flag[k] == t->seq)) ++k;
     *n_ready = k;
     return SV_OK;
@@ -1355,7 +1150,6 @@ extern "C" sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us) {
         }
     }
     t->final_done = true;
-    if (e->opts.fused && e->last_plan && e->last_plan->d_trace) fused_dump_trace(e->last_plan, getenv("SV_TRACE"));
     if (e->ktrace && getenv("SV_KTRACE")) {   // per-launch timeline of this step
         std::vector<unsigned long long> tr(2 * e->kmeta.size());
         if (cudaMemcpy(tr.data(), e->ktrace, tr.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
@@ -1409,7 +1203,6 @@ extern "C" sv_status sv_prefill(sv_session* s, const int32_t* tokens, int32_t n,
     std::lock_guard<std::mutex> lk(e->mu);
     if (e->poisoned) return fail(SV_E_DEVICE, "engine poisoned by an earlier CUDA error");
     if (e->inflight || s->busy) return fail(SV_E_BUSY, "a ticket is in flight");
-    if (e->opts.fused) return fail(SV_E_INVALID, "prefill runs on the per-op engine");
     if (n > e->opts.max_prefill) return fail(SV_E_CAPACITY, "n > max_prefill");
     for (int i = 0; i < n; ++i)
         if (tokens[i] < 0 || tokens[i] >= e->V) return fail(SV_E_INVALID, "token out of range");

@@ -1,5 +1,5 @@
-// gemm_epi.cuh — fused GEMM epilogues (shared by the per-op GEMM kernel and the
-// fused step kernel).  Input: an fp32 tile sOut[EPI_CHUNK tokens][128 rows] of
+// gemm_epi.cuh — fused GEMM epilogues (shared by the small-tile GEMM kernel and the
+// persistent large-tile kernel).  Input: an fp32 tile sOut[EPI_CHUNK tokens][128 rows] of
 // out[m, n0 + r] = sum_k X[m, k] W[n0 + r, k] for tokens tok0 .. tok0+15, and
 // rstd[m - m0] (RMSNorm folded: X = bf16(h * g), so out * rstd = RMSNorm(h) W^T).
 //   EPI_QKV    : RoPE (rotate-half, cos/sin table) on q and k; q -> fp32 buffer,

@@ -102,6 +102,7 @@ struct AttnArgs {
     // QKV GEMM has completed: attention is latency-bound and leaves HBM idle
     const void* pf_ptr = nullptr;
     size_t pf_bytes = 0;
+    int num_sms = 0;      // SMs of the engine's device (occupancy choice of attn3)
 };
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st);
 // v3 (head_dim 128): mma.sync bf16 tensor-core tiles, per-warp cp.async rings,

@@ -45,7 +45,7 @@ class sv_adapters(C.Structure):
 
 class sv_engine_opts(C.Structure):
     _fields_ = [("max_batch", C.c_int32), ("max_gamma", C.c_int32), ("use_graphs", C.c_int32),
-                ("fused", C.c_int32), ("max_prefill", C.c_int32)]
+                ("max_prefill", C.c_int32)]
 
 
 class sv_verify_req(C.Structure):
@@ -77,7 +77,7 @@ class sv_kernel_prof(C.Structure):
 
 
 KERNEL_KINDS = ["embed", "gemm_qkv", "attention", "gemm_o", "gemm_gate_up", "gemm_down",
-                "gemm_lm_exit", "accept_exit", "gemm_lm_final", "accept_final", "fused_step"]
+                "gemm_lm_exit", "accept_exit", "gemm_lm_final", "accept_final"]
 
 EXPORTS = {
     # name: (restype, argtypes)
@@ -363,8 +363,7 @@ class Ticket:
 
 class Engine:
     def __init__(self, mc, weights: Weights, max_batch: int = 1, max_gamma: int = 8,
-                 kv_blocks: int = None, use_graphs: bool = True, device: int = 0, fused: bool = None,
-                 max_prefill: int = 0):
+                 kv_blocks: int = None, use_graphs: bool = True, device: int = 0, max_prefill: int = 0):
         import torch
         self.mc = mc
         self.device = device
@@ -374,10 +373,7 @@ class Engine:
         if kv_blocks is None:
             kv_blocks = max_batch * ((mc.max_ctx + mc.page_tokens - 1) // mc.page_tokens + 1)
         self.kv_pool = torch.empty(blk * kv_blocks, dtype=torch.uint8, device=f"cuda:{device}")
-        if fused is None:
-            fused = os.environ.get("SV_FUSED", "0") == "1"
-        opts = sv_engine_opts(max_batch, max_gamma, 1 if use_graphs else 0, 1 if fused else 0, max_prefill)
-        self.fused = bool(fused)
+        opts = sv_engine_opts(max_batch, max_gamma, 1 if use_graphs else 0, max_prefill)
         h = C.c_void_p()
         check(lib().sv_engine_create(C.byref(self.cfg), C.byref(weights.w), C.byref(opts), device,
                                      C.c_void_p(self.kv_pool.data_ptr()), blk * kv_blocks, C.byref(h)))

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol(svlib):
 
 def test_status_strings(svlib):
     assert sv.status_name(sv.SV_E_PROTOCOL) == "SV_E_PROTOCOL"
-    assert svlib.sv_abi_version() == 2
+    assert svlib.sv_abi_version() == 3
 
 
 def test_pure_host_calls(svlib):
@@ -57,6 +57,6 @@ def test_no_cpu_fallback(svlib):
     cfg = sv.make_cfg(tiny())
     h = C.c_void_p()
     w = sv.sv_weights()
-    opts = sv.sv_engine_opts(1, 4, 1, 1)
+    opts = sv.sv_engine_opts(1, 4, 1, 0)
     s = svlib.sv_engine_create(C.byref(cfg), C.byref(w), C.byref(opts), 0, C.c_void_p(1), 1 << 20, C.byref(h))
     assert s == sv.SV_E_DEVICE

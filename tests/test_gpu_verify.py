@@ -20,17 +20,17 @@ pytestmark = pytest.mark.gpu
 LOGIT_TOL = 2e-2
 
 
-def _setup(mc, B, max_gamma=8, use_graphs=True, fused=None):
+def _setup(mc, B, max_gamma=8, use_graphs=True):
     from paper_2505_21594_b200 import sv
     W = sv.Weights(mc, seed=1)
-    eng = sv.Engine(mc, W, max_batch=B, max_gamma=max_gamma, use_graphs=use_graphs, fused=fused)
+    eng = sv.Engine(mc, W, max_batch=B, max_gamma=max_gamma, use_graphs=use_graphs)
     return sv, W, eng
 
 
-def _run_rounds(mc, B, gamma, ctx, exit_layer, greedy, rounds, use_graphs=True, model=None, fused=None):
+def _run_rounds(mc, B, gamma, ctx, exit_layer, greedy, rounds, use_graphs=True, model=None):
     """Run `rounds` verify steps on B sessions through libsv and the oracle in
     lockstep (each side keeps its own cache); returns the tally and errors."""
-    sv, W, eng = _setup(mc, B, use_graphs=use_graphs, fused=fused)
+    sv, W, eng = _setup(mc, B, use_graphs=use_graphs)
     model = model or om.Model(mc, seed=1)
     gs, os_ = [], []
     for b in range(B):
@@ -75,33 +75,30 @@ def _run_rounds(mc, B, gamma, ctx, exit_layer, greedy, rounds, use_graphs=True, 
     return tally_f, tally_e, np.array(errs)
 
 
-@pytest.mark.parametrize("fused", [True, False], ids=["fused", "per_op"])
 @pytest.mark.parametrize("greedy", [True, False], ids=["greedy", "stochastic"])
 @pytest.mark.parametrize("ctx", [64, 59])
-def test_tiny_end_to_end(svlib, greedy, ctx, fused):
+def test_tiny_end_to_end(svlib, greedy, ctx):
     """configs[0]: 2 layers, d=128, 4 heads, V=512, ctx 64 (or 59 = 64 - G), gamma=4,
-    batch 1, early exit at layer 1; both engines (fused persistent step, per-op kernels)."""
-    tf, te, errs = _run_rounds(tiny(), 1, 4, ctx, 1, greedy, rounds=4, fused=fused)
+    batch 1, early exit at layer 1."""
+    tf, te, errs = _run_rounds(tiny(), 1, 4, ctx, 1, greedy, rounds=4)
     print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
     assert errs.max() < LOGIT_TOL
     assert not tf.hard_mismatch and not te.hard_mismatch
 
 
-@pytest.mark.parametrize("fused", [True, False], ids=["fused", "per_op"])
 @pytest.mark.parametrize("gamma", [1, 3, 8])
-def test_tiny_batched_gamma_sweep(svlib, gamma, fused):
-    tf, te, errs = _run_rounds(tiny(), 5, gamma, 37, 2, False, rounds=2, fused=fused)
+def test_tiny_batched_gamma_sweep(svlib, gamma):
+    tf, te, errs = _run_rounds(tiny(), 5, gamma, 37, 2, False, rounds=2)
     print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
     assert errs.max() < LOGIT_TOL
     assert not tf.hard_mismatch and not te.hard_mismatch
 
 
-@pytest.mark.parametrize("fused", [True, False], ids=["fused", "per_op"])
-def test_tiny_large_batch(svlib, fused):
+def test_tiny_large_batch(svlib):
     """B = 60 requests (M = 300 query rows): the 256-token GEMM tile with two token
     tiles, the batched attention grid and 60 acceptance instances (configs[3]-style
     batching at the tiny shape)."""
-    tf, te, errs = _run_rounds(tiny(), 60, 4, 40, 1, False, rounds=2, fused=fused)
+    tf, te, errs = _run_rounds(tiny(), 60, 4, 40, 1, False, rounds=2)
     print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
     assert errs.max() < LOGIT_TOL
     assert not tf.hard_mismatch and not te.hard_mismatch
@@ -195,8 +192,8 @@ def test_rollback_bit_exact(svlib):
     eng.close()
 
 
-@pytest.mark.parametrize("shape,fused", [("tiny", False), ("tiny", True), ("7b_width", False)])
-def test_poisoned_kv_tail_is_invisible(svlib, shape, fused):
+@pytest.mark.parametrize("shape", ["tiny", "7b_width"])
+def test_poisoned_kv_tail_is_invisible(svlib, shape):
     """DESIGN.md R22 (iii): KV slots at or beyond the cached length hold arbitrary
     bits (here all-NaN bf16 0xFFFF) without changing a step: results and logits are
     bitwise equal to a run on a zeroed pool."""
@@ -206,7 +203,7 @@ def test_poisoned_kv_tail_is_invisible(svlib, shape, fused):
     W = sv.Weights(mc, seed=1)
     outs = []
     for fill in (0, 255):
-        eng = sv.Engine(mc, W, max_batch=2, max_gamma=8, fused=fused)
+        eng = sv.Engine(mc, W, max_batch=2, max_gamma=8)
         eng.kv_pool.fill_(fill)
         ss = [eng.open_session(1 + b, 7 + b) for b in range(2)]
         for b, s in enumerate(ss):
@@ -262,12 +259,11 @@ def test_host_probs_equal_device_probs(svlib):
     eng.close()
 
 
-@pytest.mark.parametrize("fused", [True, False], ids=["fused", "per_op"])
-def test_7b_width_two_layers(svlib, fused):
+def test_7b_width_two_layers(svlib):
     """Llama2-7B layer shapes (d=4096, 32 heads, F=11008, V=32000) with 2 layers,
     batch 2, ctx 200: logits and decisions vs the fp64 oracle."""
     mc = ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=512)
-    tf, te, errs = _run_rounds(mc, 2, 4, 200, 1, False, rounds=2, fused=fused)
+    tf, te, errs = _run_rounds(mc, 2, 4, 200, 1, False, rounds=2)
     print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
     assert errs.max() < LOGIT_TOL
     assert not tf.hard_mismatch and not te.hard_mismatch

@@ -120,3 +120,70 @@ def test_all_exits_match_single_exit_runs():
         assert r.score == single.early.score
     le, r, z = out.exits[-1]
     assert np.array_equal(z, out.final_logits) and r.tokens == out.final.tokens
+
+
+# --------------------------------------------------------------------------------
+# prefill_step pinned against HF LlamaForCausalLM float64
+# (library routine): the next token of a prompt is HF's last-row argmax, the
+# kept K/V rows are HF's cache, a continued prefill equals one pass over the
+# whole prompt, and the sampled next token follows softmax of HF's last row.
+# --------------------------------------------------------------------------------
+import pytest
+from scipy import stats
+
+from oracle.verify import prefill_step
+from .test_oracle_model import _hf_model
+
+
+def _hf_run(cfg, m, seq):
+    import torch
+    hf = _hf_model(cfg, m)
+    with torch.no_grad():
+        out = hf(torch.from_numpy(np.asarray(seq))[None], use_cache=True)
+    return hf, out
+
+
+def test_prefill_matches_hf_greedy_and_cache():
+    cfg = tiny()
+    m = om.Model(cfg, 1)
+    seq = np.random.default_rng(31).integers(0, cfg.vocab, size=40)
+    _, out = _hf_run(cfg, m, seq)
+    z_hf = out.logits[0].numpy()
+    s = Session(3, 9, om.KVCache(cfg))
+    res, zl = prefill_step(m, s, 1, seq)
+    assert np.max(np.abs(zl[0] - z_hf[-1])) < 1e-6 * np.max(np.abs(z_hf[-1]))
+    assert res.accepted == 0 and res.tokens == [int(np.argmax(z_hf[-1]))]
+    assert s.cache.length == 40 and s.last_round == 1
+    for l in range(cfg.n_layers):
+        k_hf = out.past_key_values.layers[l].keys[0].numpy()      # [H, T, Dh], after RoPE
+        v_hf = out.past_key_values.layers[l].values[0].numpy()
+        assert np.max(np.abs(s.cache.k[l] - k_hf)) < 1e-6 * np.max(np.abs(k_hf))
+        assert np.max(np.abs(s.cache.v[l] - v_hf)) < 1e-6 * np.max(np.abs(v_hf))
+    # a continued prefill (25 then 15 tokens) equals the single pass
+    s2 = Session(3, 9, om.KVCache(cfg))
+    prefill_step(m, s2, 1, seq[:25])
+    res2, zl2 = prefill_step(m, s2, 2, seq[25:])
+    assert np.max(np.abs(zl2[0] - z_hf[-1])) < 1e-6 * np.max(np.abs(z_hf[-1]))
+    assert res2.tokens == res.tokens and s2.cache.length == 40
+    with pytest.raises(ValueError):
+        prefill_step(m, s2, 7, seq[:3])                             # round 7 is not 2 + 1
+
+
+def test_prefill_sampled_token_follows_hf_last_row():
+    cfg = tiny()
+    m = om.Model(cfg, 2)
+    seq = np.array([5, 77, 300])
+    _, out = _hf_run(cfg, m, seq)
+    p = acc.softmax(out.logits[0, -1].numpy())
+    N = 3000
+    counts = np.zeros(cfg.vocab)
+    for r in range(1, N + 1):
+        s = Session(4, 11, om.KVCache(cfg), last_round=r - 1)
+        res, _ = prefill_step(m, s, r, seq, sample=True)
+        assert res.accepted == 0 and len(res.tokens) == 1
+        counts[res.tokens[0]] += 1
+    big = N * p >= 5
+    obs = np.append(counts[big], counts[~big].sum())
+    exp = np.append(N * p[big], N * p[~big].sum())
+    assert big.sum() >= 3
+    assert stats.chisquare(obs, exp).pvalue > 1e-3
