@@ -108,6 +108,27 @@ def attention(q, K, V, ctx: int) -> np.ndarray:
     return out
 
 
+def decoder_layer(cfg, w: dict, cache: KVCache, l: int, h: np.ndarray, pos: np.ndarray) -> np.ndarray:
+    """One decoder layer f^(l) (Eq. 3) on the block h [G, d] at
+    positions pos (cache rows 0..pos[0]-1 are the cached context); appends the
+    block's K/V rows to layer l of `cache` and returns h^(l+1)."""
+    H, Dh = cfg.n_heads, cfg.head_dim
+    G = h.shape[0]
+    ctx = int(pos[0])
+    x = rms_norm(h, w["g_attn"], cfg.rms_eps)
+    q = (x @ w["wq"].T).reshape(G, H, Dh)
+    k = (x @ w["wk"].T).reshape(G, H, Dh)
+    v = (x @ w["wv"].T).reshape(G, H, Dh)
+    q = rope(q, pos, cfg.rope_theta)
+    k = rope(k, pos, cfg.rope_theta)
+    cache.k[l] = np.concatenate([cache.k[l][:, :ctx, :], k.transpose(1, 0, 2)], axis=1)
+    cache.v[l] = np.concatenate([cache.v[l][:, :ctx, :], v.transpose(1, 0, 2)], axis=1)
+    a = attention(q, cache.k[l], cache.v[l], ctx).reshape(G, H * Dh)
+    h = h + a @ w["wo"].T
+    x = rms_norm(h, w["g_mlp"], cfg.rms_eps)
+    return h + (silu(x @ w["wg"].T) * (x @ w["wu"].T)) @ w["wdown"].T
+
+
 def forward(model: Model, cache: KVCache, tokens: np.ndarray, exit_layer: int = 0):
     """Run the query block `tokens` (positions cache.length ..) through all layers.
 
@@ -115,34 +136,31 @@ def forward(model: Model, cache: KVCache, tokens: np.ndarray, exit_layer: int = 
     the caller rolls back).  Returns (final_logits [G, V], exit_logits [G, V] or None,
     hidden states list h^(0..L) [G, d]).
     """
+    return forward_many(model, [cache], [tokens], exit_layer)[0]
+
+
+def forward_many(model: Model, caches, blocks, exit_layer: int = 0):
+    """`forward` for several independent sessions (cache_i, block_i): the layer loop
+    is outermost so a lazily generated layer is built once for all of them; each
+    session's arithmetic is exactly `forward`'s.  Returns a list of
+    (final_logits, exit_logits, hidden states) per session."""
     cfg = model.cfg
-    H, Dh = cfg.n_heads, cfg.head_dim
-    tokens = np.asarray(tokens, dtype=np.int64)
-    G = len(tokens)
-    ctx = cache.length
-    pos = np.arange(ctx, ctx + G)
-    h = model.glob["embed"][tokens].copy()                 # h^(0), Eq. 3
-    hs = [h.copy()]
-    exit_logits = None
+    blocks = [np.asarray(t, dtype=np.int64) for t in blocks]
+    ctxs = [c.length for c in caches]
+    poss = [np.arange(ctx, ctx + len(t)) for ctx, t in zip(ctxs, blocks)]
+    hs = [model.glob["embed"][t].copy() for t in blocks]   # h^(0), Eq. 3
+    hist = [[h.copy()] for h in hs]
+    exit_logits = [None] * len(blocks)
     for l in range(cfg.n_layers):
         w = model.layer(l)
-        x = rms_norm(h, w["g_attn"], cfg.rms_eps)
-        q = (x @ w["wq"].T).reshape(G, H, Dh)
-        k = (x @ w["wk"].T).reshape(G, H, Dh)
-        v = (x @ w["wv"].T).reshape(G, H, Dh)
-        q = rope(q, pos, cfg.rope_theta)
-        k = rope(k, pos, cfg.rope_theta)
-        cache.k[l] = np.concatenate([cache.k[l][:, :ctx, :], k.transpose(1, 0, 2)], axis=1)
-        cache.v[l] = np.concatenate([cache.v[l][:, :ctx, :], v.transpose(1, 0, 2)], axis=1)
-        a = attention(q, cache.k[l], cache.v[l], ctx).reshape(G, H * Dh)
-        h = h + a @ w["wo"].T
-        x = rms_norm(h, w["g_mlp"], cfg.rms_eps)
-        h = h + (silu(x @ w["wg"].T) * (x @ w["wu"].T)) @ w["wdown"].T
-        hs.append(h.copy())
-        if exit_layer and l + 1 == exit_layer:
-            exit_logits = lm_head(model, h)
-    cache.length = ctx + G
-    return lm_head(model, h), exit_logits, hs
+        for i, cache in enumerate(caches):
+            hs[i] = decoder_layer(cfg, w, cache, l, hs[i], poss[i])
+            hist[i].append(hs[i].copy())
+            if exit_layer and l + 1 == exit_layer:
+                exit_logits[i] = lm_head(model, hs[i])
+    for cache, ctx, t in zip(caches, ctxs, blocks):
+        cache.length = ctx + len(t)
+    return [(lm_head(model, hs[i]), exit_logits[i], hist[i]) for i in range(len(blocks))]
 
 
 class Adapters:

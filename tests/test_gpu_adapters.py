@@ -16,7 +16,7 @@ from workload import drafts as wd
 from workload import tiny
 from workload.configs import ModelCfg
 
-from .gpu_helpers import Tally, decision_bound, oracle_session, row_rel_err
+from .gpu_helpers import Tally, oracle_session, row_rel_err, save_report
 
 pytestmark = pytest.mark.gpu
 
@@ -71,7 +71,7 @@ def test_exit_adapters_against_oracle(svlib, shape):
 
     _, f_plain, _, zf_plain = run(exit_layer=1)
     eng.set_adapters(A)
-    tally = Tally()
+    tally = Tally("adapters")
     for le in range(1, L):
         got, f, ze, zf = run(exit_layer=le)
         assert np.array_equal(zf, zf_plain)                       # exits are read-only
@@ -84,7 +84,7 @@ def test_exit_adapters_against_oracle(svlib, shape):
             plain = verify_step(model, oracle_session(mc, model, 50 + b, 600 + b, 21 + b, ctx), 1, 13 + b, x[b],
                                 q[b].astype(np.float64), exit_layer=le)
             assert not np.allclose(out.exit_logits, plain.exit_logits)   # the adapter acts
-            tally.add(out.early, got[0][b], decision_bound(eps.max()), tag=(le, b))
+            tally.add(out.early, got[0][b], out.exit_logits, eps, q[b], (600 + b, 50 + b, 1), tag=(le, b))
     # the all-exits stream with adapters: exit k equals the single-exit run of that layer
     exits = list(range(1, L + 1))
     got_all, _, _, _ = run(exits=exits)
@@ -92,6 +92,7 @@ def test_exit_adapters_against_oracle(svlib, shape):
         single, _, _, _ = run(exit_layer=le)
         assert [r.asdict() for r in got_all[k]] == [r.asdict() for r in single[0]]
     print(tally.report())
-    assert not tally.hard_mismatch
+    save_report(tally.name, tally.asdict())
+    assert not tally.hard_mismatch and tally.checked >= 1
     eng.set_adapters(None)
     eng.close()

@@ -12,7 +12,7 @@ from oracle.verify import verify_step
 from workload import tiny
 from workload.configs import ModelCfg
 
-from .gpu_helpers import Tally, decision_bound, oracle_session, row_rel_err
+from .gpu_helpers import Tally, oracle_session, row_rel_err, save_report
 
 pytestmark = pytest.mark.gpu
 
@@ -35,13 +35,14 @@ def test_ar_decode_against_oracle(svlib, shape, greedy):
         gs.append(s)
         os_.append(oracle_session(mc, model, 40 + b, 900 + b, 11 + b, ctx))
     pending = [17 + b for b in range(B)]
-    tally, tally_e = Tally(), Tally()
+    tally, tally_e = Tally("ar_final"), Tally("ar_exit")
     for rnd in range(1, rounds + 1):
         reqs = [sv.Request(gs[b], rnd, pending[b], [], None if greedy else dummy) for b in range(B)]
         t = eng.submit(reqs, exit_layer=1)
         early = t.wait_early()
         final = t.wait_final()
         zf = t.logits(1, 0).cpu().numpy()
+        ze = t.logits(0, 0).cpu().numpy()
         t.release()
         for b in range(B):
             out = verify_step(model, os_[b], rnd, pending[b], [], None if greedy else np.zeros((0, mc.vocab)),
@@ -49,8 +50,11 @@ def test_ar_decode_against_oracle(svlib, shape, greedy):
             rel, eps = row_rel_err(zf[b], out.final_logits)
             assert rel.max() < 2e-2
             assert final[b].accepted == 0 and len(final[b].emitted()) == 1
-            tally.add(out.final, final[b], decision_bound(eps.max()), tag=(rnd, b))
-            tally_e.add(out.early, early[b], decision_bound(4 * eps.max()), tag=("exit", rnd, b))
+            rel_e, eps_e = row_rel_err(ze[b], out.exit_logits)
+            assert rel_e.max() < 2e-2
+            ctr = (900 + b, 40 + b, rnd)
+            tally.add(out.final, final[b], out.final_logits, eps, None, ctr, tag=(rnd, b))
+            tally_e.add(out.early, early[b], out.exit_logits, eps_e, None, ctr, tag=("exit", rnd, b))
             assert gs[b].length == ctx + rnd
             if out.final.tokens == final[b].emitted():
                 pending[b] = final[b].emitted()[0]
@@ -60,6 +64,7 @@ def test_ar_decode_against_oracle(svlib, shape, greedy):
             break
     print(tally.report(), "|", tally_e.report())
     assert not tally.hard_mismatch and not tally_e.hard_mismatch
+    assert tally.checked >= 0.5 * tally.n
     for s in gs:
         s.close()
     eng.close()

@@ -14,7 +14,7 @@ from workload import drafts as wd
 from workload import tiny
 from workload.configs import ModelCfg
 
-from .gpu_helpers import Tally, decision_bound, oracle_session, row_rel_err
+from .gpu_helpers import Tally, oracle_session, row_rel_err, save_report
 
 pytestmark = pytest.mark.gpu
 
@@ -71,12 +71,15 @@ def test_all_exits_against_oracle_and_single_exit(svlib, shape, greedy):
         s.close()
     assert np.array_equal(z0, zf)
     assert [r.asdict() for r in f0] == [r.asdict() for r in final]
-    # 3. every exit equals the single-exit run of that layer, bitwise
+    # 3. every exit equals the single-exit run of that layer, bitwise (whose exit
+    # logits are downloaded for the oracle comparison below)
+    ze = {}
     for k, le in enumerate(exits):
         ss = fresh()
         t = eng.submit(reqs(ss), exit_layer=le)
         e1 = t.wait_early()
         t.wait_final()
+        ze[le] = t.logits(0, gamma).cpu().numpy()
         t.release()
         for s in ss:
             s.close()
@@ -90,17 +93,21 @@ def test_all_exits_against_oracle_and_single_exit(svlib, shape, greedy):
         for key in ("accepted", "tokens", "score", "next_prob", "status"):
             assert e[key] == f[key], key
     # 4. against the oracle: every exit's decisions (margin-binned)
-    tally = Tally()
+    tally = Tally(f"all_exits_{shape}_{'greedy' if greedy else 'stochastic'}")
     for b in range(B):
         osess = oracle_session(mc, model, 30 + b, 500 + b, 7 + b, ctx)
         out = verify_step(model, osess, 1, 11 + b, x[b], None if greedy else q[b].astype(np.float64),
                           exit_layers=exits)
         rel, eps = row_rel_err(zf[b], out.final_logits)
         assert rel.max() < 2e-2
-        for k, (le, r, _) in enumerate(out.exits):
-            tally.add(r, got[k][b], decision_bound(2 * eps.max()), tag=(le, b))
+        for k, (le, r, zl) in enumerate(out.exits):
+            rel_l, eps_l = row_rel_err(ze[le][b], zl)
+            assert rel_l.max() < 2e-2
+            tally.add(r, got[k][b], zl, eps_l, None if greedy else q[b], (500 + b, 30 + b, 1), tag=(le, b))
     print(tally.report())
+    save_report(tally.name, tally.asdict())
     assert not tally.hard_mismatch, tally.hard_mismatch
+    assert tally.checked >= (0.75 if shape == "tiny4" else 0.3) * tally.n
     eng.close()
 
 

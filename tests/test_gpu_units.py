@@ -12,7 +12,7 @@ from workload import drafts as wd
 from workload import tiny
 from workload.configs import ModelCfg
 
-from .gpu_helpers import Tally
+from .gpu_helpers import Tally, save_report
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "philox_kat.txt")
@@ -104,16 +104,17 @@ def test_accept_matches_oracle_on_identical_logits(svlib, V, greedy):
     W = sv.Weights(mc, seed=1)
     eng = sv.Engine(mc, W, max_batch=8, max_gamma=8)
     sessions = [eng.open_session(100 + b, 0x1234 + 77 * b) for b in range(8)]
-    tally = Tally()
+    tally = Tally(f"level_u_V{V}_{'greedy' if greedy else 'stochastic'}")
     for gamma in (1, 2, 4, 8):
         for seed in range(6):
             refs, got = _accept_case(eng, mc, 8, gamma, seed * 10 + gamma, greedy, sessions)
             for r, g in zip(refs, got):
-                tally.add(r, g, 1e-3, tag=(gamma, seed))
+                tally.add_fixed(r, g, 1e-3, tag=(gamma, seed))
                 if r.status == oacc.OK and r.tokens == g.emitted():
                     assert abs(g.score - r.score) <= 1e-5 * max(1.0, r.score)
                     assert abs(g.next_prob - r.next_prob) <= 1e-4 * max(1e-3, r.next_prob)
     print(tally.report())
+    save_report(tally.name, tally.asdict())
     assert not tally.hard_mismatch, tally.hard_mismatch[:3]
     assert tally.checked >= 0.9 * tally.n
     for s in sessions:

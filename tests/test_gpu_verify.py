@@ -14,7 +14,7 @@ from workload import drafts as wd
 from workload import tiny
 from workload.configs import ModelCfg
 
-from .gpu_helpers import Tally, decision_bound, oracle_session, row_rel_err
+from .gpu_helpers import Tally, UTally, oracle_session, row_rel_err, save_report
 
 pytestmark = pytest.mark.gpu
 LOGIT_TOL = 2e-2
@@ -39,7 +39,7 @@ def _run_rounds(mc, B, gamma, ctx, exit_layer, greedy, rounds, use_graphs=True, 
         gs.append(s)
         os_.append(oracle_session(mc, model, 10 + b, 1000 + b, 2 + b, ctx))
     pending = list(wd.prefix_tokens(3, B, mc.vocab))
-    tally_f, tally_e = Tally(), Tally()
+    tally_f, tally_e = Tally("final"), Tally("exit")
     errs = []
     for rnd in range(1, rounds + 1):
         x, q = wd.timing_drafts(100 + rnd, B, gamma, mc.vocab, s=1.1)
@@ -56,11 +56,13 @@ def _run_rounds(mc, B, gamma, ctx, exit_layer, greedy, rounds, use_graphs=True, 
                               exit_layer=exit_layer)
             rel, eps = row_rel_err(zf[b], out.final_logits)
             errs.append(rel.max())
-            tally_f.add(out.final, final[b], decision_bound(eps.max()), tag=("final", rnd, b))
+            qb = None if greedy else q[b]
+            ctr = (1000 + b, 10 + b, rnd)
+            tally_f.add(out.final, final[b], out.final_logits, eps, qb, ctr, tag=("final", rnd, b))
             if exit_layer:
                 rel_e, eps_e = row_rel_err(ze[b], out.exit_logits)
                 errs.append(rel_e.max())
-                tally_e.add(out.early, early[b], decision_bound(eps_e.max()), tag=("exit", rnd, b))
+                tally_e.add(out.early, early[b], out.exit_logits, eps_e, qb, ctr, tag=("exit", rnd, b))
             assert gs[b].length == final[b].new_len
             if out.final.status == oacc.OK and out.final.tokens == final[b].emitted():
                 assert final[b].new_len == out.new_len
@@ -82,8 +84,11 @@ def test_tiny_end_to_end(svlib, greedy, ctx):
     batch 1, early exit at layer 1."""
     tf, te, errs = _run_rounds(tiny(), 1, 4, ctx, 1, greedy, rounds=4)
     print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
+    save_report(f"tiny_e2e_{'greedy' if greedy else 'stochastic'}_ctx{ctx}",
+                dict(final=tf.asdict(), exit=te.asdict(), max_rel_logit_err=float(errs.max())))
     assert errs.max() < LOGIT_TOL
     assert not tf.hard_mismatch and not te.hard_mismatch
+    assert tf.checked >= 0.75 * tf.n and te.checked >= 0.75 * te.n
 
 
 @pytest.mark.parametrize("gamma", [1, 3, 8])
@@ -92,6 +97,7 @@ def test_tiny_batched_gamma_sweep(svlib, gamma):
     print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
     assert errs.max() < LOGIT_TOL
     assert not tf.hard_mismatch and not te.hard_mismatch
+    assert tf.checked >= 0.75 * tf.n and te.checked >= 0.75 * te.n
 
 
 def test_tiny_large_batch(svlib):
@@ -100,8 +106,10 @@ def test_tiny_large_batch(svlib):
     batching at the tiny shape)."""
     tf, te, errs = _run_rounds(tiny(), 60, 4, 40, 1, False, rounds=2)
     print("final:", tf.report(), "| exit:", te.report(), "| max rel logit err", errs.max())
+    save_report("tiny_large_batch", dict(final=tf.asdict(), exit=te.asdict(), max_rel_logit_err=float(errs.max())))
     assert errs.max() < LOGIT_TOL
     assert not tf.hard_mismatch and not te.hard_mismatch
+    assert tf.checked >= 0.75 * tf.n and te.checked >= 0.75 * te.n
 
 
 @pytest.mark.parametrize("shape", ["tiny", "7b_width"])
@@ -154,18 +162,24 @@ def test_exit_is_side_effect_free(svlib):
     eng.close()
 
 
-def test_rollback_bit_exact(svlib):
+@pytest.mark.parametrize("shape", ["tiny", "7b_width"])
+def test_rollback_bit_exact(svlib, shape):
     """DESIGN.md R22: (i) rows [0, ctx) byte-identical across a step; (ii) two steps
     that differ only in the rejected suffix leave byte-identical visible caches and
-    byte-identical next steps; (iv) length == ctx + 1 + delta."""
-    mc = tiny()
+    byte-identical next steps; (iv) length == ctx + 1 + delta.  The 7B-width case
+    (2 layers, ctx 300, one request) runs split-K GEMMs and split-KV attention."""
+    if shape == "tiny":
+        mc, ctx = tiny(), 30
+    else:
+        mc, ctx = ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=512), 300
     sv, W, eng = _setup(mc, 1)
     model = om.Model(mc, seed=1)
-    ctx = 30
     # the target's greedy continuation from the oracle (an input, not a GPU value)
     osess = oracle_session(mc, model, 1, 1, 4, ctx)
-    c = osess.cache.copy()
-    z, _, _ = om.forward(model, c, [7])
+    for pend in range(7, 40):        # a pending token whose greedy successor has a clear top-2 gap
+        z, _, _ = om.forward(model, osess.cache.copy(), [pend])
+        if oacc.top2_gap(z[0]) > 0.2:
+            break
     a1 = int(np.argmax(z[0]))
     final_states = []
     for suffix in ([3, 3, 3], [9, 100, 200]):
@@ -173,7 +187,7 @@ def test_rollback_bit_exact(svlib):
         s.fill_kv(ctx, kv_seed=4)
         k0, v0 = s.kv_rows(0, 0, ctx)
         drafts = [a1] + [(a1 + 1 + suffix[0]) % mc.vocab] + suffix[1:]
-        _, f = eng.verify([sv.Request(s, 1, 7, drafts)], exit_layer=0)
+        _, f = eng.verify([sv.Request(s, 1, pend, drafts)], exit_layer=0)
         assert f[0].accepted == 1 and s.length == ctx + 1 + 1
         k1, v1 = s.kv_rows(0, 0, ctx)
         assert np.array_equal(k0, k1) and np.array_equal(v0, v1)
@@ -293,17 +307,23 @@ def test_7b_width_c5_batch(svlib):
     zf = t.logits(1, gamma).cpu().numpy()
     ze = t.logits(0, gamma).cpu().numpy()
     t.release()
-    tally = Tally()
+    tally = Tally("7b_width_c5_batch")
+    ut = UTally("7b_width_c5_batch level U")
+    for b in range(B):
+        ut.add(zf[b], final[b], x[b], q[b], (70 + b, 60 + b, 1), tag=("final", b))
+        ut.add(ze[b], early[b], x[b], q[b], (70 + b, 60 + b, 1), tag=("exit", b))
     for b in (0, 7, 15):
         osess = oracle_session(mc, model, 60 + b, 70 + b, 80 + b, ctx)
         out = verify_step(model, osess, 1, 5 + b, x[b], q[b].astype(np.float64), exit_layer=1)
         rel, eps = row_rel_err(zf[b], out.final_logits)
         rel_e, eps_e = row_rel_err(ze[b], out.exit_logits)
         assert rel.max() < LOGIT_TOL and rel_e.max() < LOGIT_TOL
-        tally.add(out.final, final[b], decision_bound(eps.max()), tag=("final", b))
-        tally.add(out.early, early[b], decision_bound(eps_e.max()), tag=("exit", b))
-    print(tally.report())
-    assert not tally.hard_mismatch
+        tally.add(out.final, final[b], out.final_logits, eps, q[b], (70 + b, 60 + b, 1), tag=("final", b))
+        tally.add(out.early, early[b], out.exit_logits, eps_e, q[b], (70 + b, 60 + b, 1), tag=("exit", b))
+    print(tally.report(), "|", ut.report())
+    save_report("7b_width_c5_batch", dict(level_e=tally.asdict(), level_u=ut.asdict()))
+    assert not tally.hard_mismatch and not ut.hard_mismatch
+    assert ut.checked >= 0.8 * ut.n and tally.checked >= 2
     for s in ss:
         s.close()
     eng.close()
@@ -333,18 +353,24 @@ def test_7b_width_c4_batch(svlib):
     zf = t.logits(1, gamma).cpu().numpy()
     ze = t.logits(0, gamma).cpu().numpy()
     t.release()
-    tally = Tally()
+    tally = Tally("7b_width_c4_batch")
+    ut = UTally("7b_width_c4_batch level U")
+    for b in range(0, B, 4):
+        ut.add(zf[b], final[b], x[b], q[b], (300 + b, 100 + b, 1), tag=("final", b))
+        ut.add(ze[b], early[b], x[b], q[b], (300 + b, 100 + b, 1), tag=("exit", b))
     for b in (0, 131, 255):
         osess = oracle_session(mc, model, 100 + b, 300 + b, 400 + b, ctx)
         out = verify_step(model, osess, 1, (7 * b) % mc.vocab, x[b], q[b].astype(np.float64), exit_layer=1)
         rel, eps = row_rel_err(zf[b], out.final_logits)
         rel_e, eps_e = row_rel_err(ze[b], out.exit_logits)
         assert rel.max() < LOGIT_TOL and rel_e.max() < LOGIT_TOL
-        tally.add(out.final, final[b], decision_bound(eps.max()), tag=("final", b))
-        tally.add(out.early, early[b], decision_bound(eps_e.max()), tag=("exit", b))
+        tally.add(out.final, final[b], out.final_logits, eps, q[b], (300 + b, 100 + b, 1), tag=("final", b))
+        tally.add(out.early, early[b], out.exit_logits, eps_e, q[b], (300 + b, 100 + b, 1), tag=("exit", b))
         assert ss[b].length == final[b].new_len
-    print(tally.report())
-    assert not tally.hard_mismatch
+    print(tally.report(), "|", ut.report())
+    save_report("7b_width_c4_batch", dict(level_e=tally.asdict(), level_u=ut.asdict()))
+    assert not tally.hard_mismatch and not ut.hard_mismatch
+    assert ut.checked >= 0.8 * ut.n and tally.checked >= 2
     for s in ss:
         s.close()
     eng.close()

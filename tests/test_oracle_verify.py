@@ -187,3 +187,30 @@ def test_prefill_sampled_token_follows_hf_last_row():
     exp = np.append(N * p[big], N * p[~big].sum())
     assert big.sum() >= 3
     assert stats.chisquare(obs, exp).pvalue > 1e-3
+
+
+def test_verify_steps_equals_per_session_verify_step():
+    """verify_steps (one forward over several sessions, layer loop outermost) gives
+    every session exactly verify_step's result: same logits bits, same decisions,
+    same rolled-back cache; a session with a bad round id is a protocol error and
+    does not disturb the others."""
+    from oracle.verify import verify_steps
+    cfg = tiny()
+    m = om.Model(cfg, 1)
+    x, q = timing_drafts(5, 3, 4, cfg.vocab)
+    ctxs = (20, 33, 7)
+    single = []
+    for b in range(3):
+        s = _session(cfg, m, ctx=ctxs[b], seed=10 + b, sid=b + 1, prefill=False)
+        single.append((verify_step(m, s, 1, 3 + b, x[b], q[b], exit_layer=1), s))
+    ss = [_session(cfg, m, ctx=ctxs[b], seed=10 + b, sid=b + 1, prefill=False) for b in range(3)]
+    bad = _session(cfg, m, ctx=9, seed=3, sid=9, prefill=False)
+    outs = verify_steps(m, ss + [bad], [1, 1, 1, 4], [3, 4, 5, 1], list(x) + [x[0]], list(q) + [q[0]],
+                        exit_layer=1)
+    for (ref, rs), out, s in zip(single, outs, ss):
+        assert np.array_equal(ref.final_logits, out.final_logits)
+        assert np.array_equal(ref.exit_logits, out.exit_logits)
+        assert ref.final == out.final and ref.early == out.early and ref.new_len == out.new_len
+        for l in range(cfg.n_layers):
+            assert np.array_equal(rs.cache.k[l], s.cache.k[l]) and np.array_equal(rs.cache.v[l], s.cache.v[l])
+    assert outs[3].final.status == acc.E_PROTOCOL and bad.cache.length == 9
