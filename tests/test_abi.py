@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol(svlib):
 
 def test_status_strings(svlib):
     assert sv.status_name(sv.SV_E_PROTOCOL) == "SV_E_PROTOCOL"
-    assert svlib.sv_abi_version() == 3
+    assert svlib.sv_abi_version() == 4
 
 
 def test_pure_host_calls(svlib):
