@@ -41,7 +41,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-N_SETS = 8
+N_SETS = 64
 METRIC = "verify-step latency p50 and verified tokens/s, Llama2-7B shape gamma=4"
 UNIT = "tokens/s"
 
@@ -49,7 +49,7 @@ UNIT = "tokens/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4", "C5"])
@@ -67,6 +67,10 @@ def parse():
     ap.add_argument("--ctx", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default=None, help="write per-launch profile records here")
+    ap.add_argument("--shard", default=None, metavar="R/N",
+                    help="serve rank R's requests of an N-rank job in this single process (equality tests)")
+    ap.add_argument("--dump-results", default=None, metavar="PATH",
+                    help="write every timed step's final results per request id ({rank} is substituted)")
     return ap.parse_args()
 
 
@@ -220,44 +224,81 @@ def ncu_traffic(kind):
 
 # ---------------------------------------------------------------------------- CPU side
 class OracleSample:
-    """Oracle verify step on a bounded sample of the workload: the Llama2-7B layer
-    shapes with 1 and 2 decoder layers (+ LM heads, acceptance), B=1, timed on the
-    host cores; one 32-layer step is extrapolated as t1 + 31 * (t2 - t1).
-    Weight generation happens once, outside the timed calls."""
+    """The oracle's verify step (oracle/verify.py, numpy fp64) on the host cores, at
+    the workload's full shape: one request of the config (Llama2-7B shape, all 32
+    decoder layers, V 32000, ctx, gamma, early exit), stochastic acceptance of
+    timing-mode drafts.  Bounded sample: the 32 decoder layers cycle through
+    N_GEN generated layers (weight generation is model state, not step work, and
+    the per-layer arithmetic is the same), so a step needs 3.2 GB of fp64 layer
+    weights instead of 54 GB; the embedding / LM head are the real ones.  The KV
+    cache is copied before each timed call (outside the timed region).  Requests
+    are processed one after another, so tokens/s = tau / (seconds per request)."""
+    N_GEN = 2
 
     def __init__(self, args, ctx):
         from oracle import model as om
-        from workload.configs import ModelCfg
+        from workload import llama2_7b
         from workload.drafts import timing_drafts
         self.args, self.ctx = args, ctx
-        self.models = {}
-        for L in (1, 2):
-            mc = ModelCfg(n_layers=L, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=ctx + 64)
-            self.models[L] = (om.Model(mc, seed=1), om.KVCache.synthetic(mc, 2, ctx))
-        self.x, self.q = timing_drafts(3, 1, args.gamma, 32000)
+        self.mc = llama2_7b()
+        n_gen = self.N_GEN
+
+        class CyclicModel(om.Model):
+            def __init__(self, cfg, seed):
+                super().__init__(cfg, seed, lazy=True)
+                self.cyc = [super(CyclicModel, self).layer(i) for i in range(n_gen)]
+
+            def layer(self, l):
+                return self.cyc[l % n_gen]
+        t0 = time.perf_counter()
+        self.model = CyclicModel(self.mc, seed=1)
+        self.cache = om.KVCache.synthetic(self.mc, 2, ctx)
+        self.setup_s = time.perf_counter() - t0
+        self.x, self.q = timing_drafts(3, 1, args.gamma, self.mc.vocab)
+        self.exit_layer = 0 if args.all_exits else args.exit_layer
         self.round = 0
+        self.t = []
 
     def step(self):
+        """Seconds of one request's verify step (wall clock) and its tokens."""
         from oracle.verify import Session as OSession
         from oracle.verify import verify_step
-        t = {}
-        toks = []
         self.round += 1
-        for L, (m, cache) in self.models.items():
-            sess = OSession(1, 4, cache.copy())
-            sess.last_round = self.round - 1
-            t0 = time.perf_counter()
-            out = verify_step(m, sess, self.round, 7, self.x[0], self.q[0].astype(np.float64), exit_layer=1)
-            t[L] = time.perf_counter() - t0
-            toks.append(out.final.accepted + 1)
-        self.t = t
-        return t[1] + 31 * max(t[2] - t[1], 1e-6), float(np.mean(toks))
+        sess = OSession(1, 4, self.cache.copy())
+        sess.last_round = self.round - 1
+        t0 = time.perf_counter()
+        out = verify_step(self.model, sess, self.round, 7, self.x[0], self.q[0].astype(np.float64),
+                          exit_layer=self.exit_layer)
+        dt = time.perf_counter() - t0
+        self.t.append(dt)
+        return dt, out.final.accepted + 1
 
-    def describe(self, t32):
-        return (f"oracle verify_step (numpy fp64) at Llama2-7B layer shapes, B=1, ctx {self.ctx}, "
-                f"gamma {self.args.gamma}, exit at layer 1, timed with 1 and 2 decoder layers "
-                f"({self.t[1]:.2f} s, {self.t[2]:.2f} s); 32-layer step extrapolated t1 + 31*(t2-t1) = "
-                f"{t32:.2f} s; weight generation excluded")
+    def describe(self):
+        return (f"oracle verify_step (numpy fp64) of one request at the full Llama2-7B shape (32 decoder layers "
+                f"cycling {self.N_GEN} generated layers' weights, real embedding and LM head), ctx {self.ctx}, "
+                f"gamma {self.args.gamma}, exit at layer {self.exit_layer}, stochastic acceptance; "
+                f"{len(self.t)} timed step(s), {np.mean(self.t):.2f} s per request; weight / KV generation "
+                f"({self.setup_s:.1f} s) and the cache copy excluded; requests are processed sequentially")
+
+
+def host_identity():
+    """CPU model and BLAS library of the host the oracle ran on."""
+    cpu = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = ", ".join(f"{i.get('internal_api')} {i.get('version')} ({i.get('num_threads')} threads)"
+                         for i in threadpool_info())
+    except Exception:
+        pass
+    return {"cpu_model": cpu, "blas": blas, "logical_cpus": os.cpu_count()}
 
 
 def expected_tau(gamma, alpha):
@@ -293,29 +334,86 @@ def run_reference(args):
     _keep = _all_host_threads()
     per, total, ctx, scaling = workload(args, 1)
     sample = OracleSample(args, ctx)
-    times, toks = [], []
+    times = []
     for i in range(args.warmup + args.steps):
-        t32, tps = sample.step()
+        dt, _ = sample.step()
         if i >= args.warmup:
-            times.append(t32)
-            toks.append(tps)
+            times.append(dt)
     sec = float(np.mean(times))
     tok = expected_tau(args.gamma, args.alpha)
-    value = per * tok / sec
-    cores, desc = host_cores(), sample.describe(sec)
+    value = tok / sec
+    cores, desc = host_cores(), sample.describe()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3 * per, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} Llama2-7B shape, B={per}, ctx {ctx}, gamma {args.gamma}",
                        "global_batch": per, "seq_len": ctx, "parallelism": "host cores"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": desc + f"; tokens/step {tok:.3f} = expected tau of the calibrated "
-                                       f"workload (alpha {args.alpha}, gamma {args.gamma})"},
+                             "sample": desc + f"; ms_per_step = {per} request(s) x {sec * 1e3:.0f} ms; tokens/step "
+                                       f"{tok:.3f} = expected tau of the calibrated workload (alpha {args.alpha}, "
+                                       f"gamma {args.gamma})", "host": host_identity()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------- GPU side
+def trace_roofline(trace, prof, hbm, tc, peak_src):
+    """Roofline of the dominant kernel family (the main-stream weight GEMMs) in a
+    step as it runs in production (graph replay with PDL; sv_debug_trace_*).
+
+    Launches on the main stream form one dependent chain; launch i is charged the
+    time from the end of the chain before it to its own end (its CTAs may start
+    earlier under PDL, but only this part is on the step's critical path), so the
+    charged times of the chain add up to the traced step.  achieved = algorithmic
+    bytes (or flops) of the family / its charged time.  Bytes and flops per launch
+    come from sv_debug_profile_step records, which list the same launches in the
+    same order.  The exit stream runs beside the chain and is reported apart."""
+    if len(trace) != len(prof) or any(t["kind"] != p["kind"] for t, p in zip(trace, prof)):
+        return None
+    step_us = max(t["end_us"] for t in trace) - min(t["start_us"] for t in trace)
+    prev = None
+    fam = {}
+    for t, p in zip(trace, prof):
+        if t["stream"] != 0:
+            key = t["kind"] + " (exit stream)"
+            charged = t["end_us"] - t["start_us"]
+        else:
+            key = t["kind"]
+            charged = t["end_us"] - (t["start_us"] if prev is None else prev)
+            prev = t["end_us"] if prev is None else max(prev, t["end_us"])
+        f = fam.setdefault(key, {"launches": 0, "us": 0.0, "bytes": 0.0, "flops": 0.0})
+        f["launches"] += 1
+        f["us"] += charged
+        f["bytes"] += p["bytes"]
+        f["flops"] += p["flops"]
+    g = [f for k, f in fam.items() if k.startswith("gemm") and "exit" not in k]
+    g_us = sum(f["us"] for f in g)
+    g_bytes = sum(f["bytes"] for f in g)
+    g_flops = sum(f["flops"] for f in g)
+    g_n = sum(f["launches"] for f in g)
+    ridge = tc * 1e12 / (hbm * 1e9)            # flops per byte where the two roofs meet
+    tensor = g_flops / g_bytes > ridge
+    if tensor:
+        achieved, peak, unit = g_flops / (g_us * 1e-6) / 1e12, tc, "TFLOP/s"
+        src = peak_src + " (bf16_tflops_sustained: the GEMMs run inside a long step)"
+    else:
+        achieved, peak, unit = g_bytes / (g_us * 1e-6) / 1e9, hbm, "GB/s"
+        src = peak_src + " (hbm_gbs)"
+    return {"bound": "tensor" if tensor else "hbm",
+            "kernel": "gemm_kernel / gemm_big_kernel (QKV, O, gate-up, down, final LM head; tcgen05 + TMA)",
+            "achieved": round(achieved, 1), "peak": peak, "unit": unit, "frac": round(achieved / peak, 4),
+            "peak_source": src, "measured_in": "one graph-replayed step with PDL (sv_debug_trace_next), "
+                                                "critical-path charge per launch",
+            "launches": g_n, "avg_launch_ms": round(g_us / g_n / 1e3, 5),
+            "algorithmic_bytes_per_launch": g_bytes / g_n, "algorithmic_flops_per_launch": g_flops / g_n,
+            "arithmetic_intensity": round(g_flops / g_bytes, 2), "ridge_flops_per_byte": round(ridge, 1),
+            "share_of_step": round(g_us / step_us, 4), "traced_step_ms": round(step_us / 1e3, 4),
+            "kernels": {k: {"launches": f["launches"], "ms": round(f["us"] / 1e3, 4),
+                            "GB/s": round(f["bytes"] / (f["us"] * 1e-6) / 1e9, 1) if f["us"] > 0 else None,
+                            "TFLOP/s": round(f["flops"] / (f["us"] * 1e-6) / 1e12, 1) if f["us"] > 0 else None}
+                        for k, f in fam.items()}}
+
+
 def run_ours(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -327,6 +425,7 @@ def run_ours(args):
         local = int(os.environ["SV_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dist = None
+    backend = None
     if world > 1:
         import torch.distributed as dist
         backend = os.environ.get("SV_DIST_BACKEND", "nccl")
@@ -334,12 +433,17 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
             dist.init_process_group(backend)
+    # --shard R/N: this process serves rank R's requests of an N-rank job on its own
+    # (the single-rank reference run of the multi-rank equality test)
+    as_rank, as_world = rank, world
+    if args.shard:
+        as_rank, as_world = (int(v) for v in args.shard.split("/"))
     from paper_2505_21594_b200 import sv
     from paper_2505_21594_b200.dist import gather_counters, shard
     from workload import llama2_7b
     from workload.drafts import prefix_tokens
 
-    per, total, ctx, scaling = workload(args, world)
+    per, total, ctx, scaling = workload(args, as_world)
     gamma, exit_layer = args.gamma, args.exit_layer
     mc = llama2_7b()
     exit_layers = list(range(1, mc.n_layers)) if args.all_exits else []
@@ -352,10 +456,11 @@ def run_ours(args):
     if args.adapters:
         eng.set_adapters(sv.Adapters(mc, args.adapters, seed=9, device=local))
     sessions = []
+    rids = list(shard(total, as_world, as_rank))   # contiguous shard of the request ids
     rounds = Rounds()
-    pend = prefix_tokens(3 + rank, per, mc.vocab)
+    pend = prefix_tokens(3 + as_rank, per, mc.vocab)
     prefill_s = []
-    for i, rid in enumerate(shard(total, world, rank)):   # contiguous shard of the request ids
+    for i, rid in enumerate(rids):
         s = eng.open_session(rid + 1, 0x5EED0000 + rid)
         if args.prefill:   # synthetic prompt of ctx uniform token ids through the model
             prompt = np.random.default_rng([5, rid]).integers(0, mc.vocab, size=ctx)
@@ -368,10 +473,12 @@ def run_ours(args):
         else:
             s.fill_kv(ctx, kv_seed=1000 + rid)
         sessions.append(s)
-    # N_SETS independent calibrated draft sets per request; step i verifies set i % N_SETS
-    n_sets = N_SETS if per <= 16 else 2
+    # independent calibrated draft sets per request, one per step until they cycle
+    # (64 at <= 16 requests per GPU, so the accepted lengths follow the workload's
+    # law rather than a few fixed draws; 8 for the 256-request pool)
+    n_sets = N_SETS if per <= 16 else 8
     sets = [build_calibrated_drafts(sv, eng, sessions, pend, ctx, gamma, args.alpha, mc.vocab,
-                                    7 + 1000 * rank + k, rounds) for k in range(n_sets)]
+                                    7 + 1000 * as_rank + k, rounds) for k in range(n_sets)]
     xs = [x for x, _ in sets]
     if gamma == 0:   # plain AR step ("Cloud AR"): sample p_0, probs pointer never read
         dummy = torch.empty(per, 1, device="cuda")
@@ -383,7 +490,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     counter = [0]
 
-    def step(host_probs=False, ev0=None):
+    def step(host_probs=False, ev0=None, timing=False):
         k = counter[0] % n_sets
         counter[0] += 1
         x = xs[k]
@@ -395,18 +502,19 @@ def run_ours(args):
             ev0.record(stream)      # and the request objects are the caller's, not the step's)
         if exit_layers:
             t = eng.submit_exits(reqs, exit_layers, stream=stream)
-            for k in range(len(exit_layers)):       # streamed: each exit as soon as it lands
-                t.wait_exit(k)
+            for j in range(len(exit_layers)):       # streamed: each exit as soon as it lands
+                t.wait_exit(j)
         else:
             t = eng.submit(reqs, exit_layer=exit_layer, stream=stream)
             if exit_layer:
                 t.wait_early()
         f = t.wait_final()
+        tm = t.timing() if timing else None
         t.release()
         bad = [r.status for r in f if r.status != sv.SV_OK]
         if bad:
             raise RuntimeError(f"verify step returned per-request errors {bad}")
-        return sum(r.accepted + 1 for r in f), f
+        return sum(r.accepted + 1 for r in f), f, tm
 
     # warm-up (also captures the CUDA graph)
     for _ in range(args.warmup):
@@ -416,18 +524,23 @@ def run_ours(args):
         dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     tokens = 0
+    per_step_tok = []
     accepted_hist = np.zeros(gamma + 2, dtype=np.int64)
+    dump = {}
     with ClockSampler(local) as clk:
         t_all0 = torch.cuda.Event(enable_timing=True)
         t_all1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         t_all0.record(stream)
         for i in range(args.steps):
-            n_tok, f = step(ev0=ev[i][0])
+            n_tok, f, _ = step(ev0=ev[i][0])
             ev[i][1].record(stream)
             tokens += n_tok
-            for r in f:
+            per_step_tok.append(n_tok / per)
+            for b, r in enumerate(f):
                 accepted_hist[r.accepted] += 1
+                if args.dump_results:
+                    dump.setdefault(rids[b], []).append(r.asdict())
         t_all1.record(stream)
         torch.cuda.synchronize()
     if dist:
@@ -443,20 +556,69 @@ def run_ours(args):
     e2e_tok = 0
     t0 = time.perf_counter()
     for i in range(args.steps):
-        n_tok, _ = step(host_probs=True)
+        n_tok, _, _ = step(host_probs=True)
         e2e_tok += n_tok
     torch.cuda.synchronize()
     e2e_el = time.perf_counter() - t0
 
-    # per-launch profile (events around each kernel, PDL off, no graph)
+    # exit-ready latency (Eq. 5; Alg-S :1103-1106): device stamps
+    # and host observation times of every exit, on separate untimed steps
+    exit_ready = None
+    if exit_layer or exit_layers:
+        tms = [step(timing=True)[2] for _ in range(min(args.steps, 30))]
+        layers = exit_layers if exit_layers else [exit_layer]
+        fin_dev = statistics.median(t["final_dev_ms"] for t in tms)
+        fin_host = statistics.median(t["final_host_ms"] for t in tms)
+        pick = range(len(layers)) if len(layers) <= 4 else [0, 7, 15, 23, len(layers) - 1]
+        exit_ready = {
+            "exit_layers": [layers[k] for k in pick],
+            "dev_ms_p50": [round(statistics.median(t["exit_dev_ms"][k] for t in tms), 4) for k in pick],
+            "host_ms_p50": [round(statistics.median(t["exit_host_ms"][k] for t in tms), 4) for k in pick],
+            "final_dev_ms_p50": round(fin_dev, 4), "final_host_ms_p50": round(fin_host, 4),
+            "model_ms": [round(layers[k] / mc.n_layers * fin_dev + 0.04, 4) for k in pick],
+            "steps": len(tms),
+            "note": "dev = first kernel start -> last request's result written (globaltimer); host = submit call "
+                    "-> mailbox flag observed by sv_wait_exit; model = (l_e / L) * final_dev + 0.04 ms "
+                    "(SURVEY.md §8(d))"}
+
+    # roofline of the timed configuration: one traced graph-replayed step (PDL on)
+    # plus the per-launch algorithmic work from a serialised profile step
+    hbm, tc, peak_src = measured_peaks()
+    eng.trace_next()
+    step()
+    trace = eng.trace_read()
     for s in sessions:
         s.rewind(ctx)
     preqs = [sv.Request(s, rounds.next(s), pend[b], xs[0][b], q_dev[0][b]) for b, s in enumerate(sessions)]
     _, recs = eng.profile_step(preqs, exit_layer=exit_layer if not exit_layers else exit_layers[len(exit_layers) // 2])
+    # per-launch algorithmic work in the traced step's launch order: main-stream
+    # launches in order; every exit's launches have the profiled exit's work
+    main_recs = [r for r in recs if r["kind"] not in ("gemm_lm_exit", "accept_exit")]
+    exit_recs = {r["kind"]: r for r in recs if r["kind"] in ("gemm_lm_exit", "accept_exit")}
+    aligned, it = [], iter(main_recs)
+    for t in trace:
+        aligned.append(next(it, None) if t["stream"] == 0 else exit_recs.get(t["kind"]))
+    roofline = None
+    step_bytes = None
+    if all(a is not None and a["kind"] == t["kind"] for a, t in zip(aligned, trace)):
+        roofline = trace_roofline(trace, aligned, hbm, tc, peak_src)
+        step_bytes = sum(a["bytes"] for a in aligned)
+    if roofline is not None:
+        roofline["traffic"] = ncu_traffic("gemm")
+        roofline["serialised_profile"] = {   # the same launches one at a time (PDL off, no graph)
+            "gemm_GB/s": round(sum(r["bytes"] for r in recs if r["kind"].startswith("gemm"))
+                               / (sum(r["ms"] for r in recs if r["kind"].startswith("gemm")) / 1e3) / 1e9, 1),
+            "step_ms": round(sum(r["ms"] for r in recs), 4)}
+        roofline["step_algorithmic_bytes"] = step_bytes
+        roofline["step_frac_of_peak"] = round(step_bytes / (statistics.median(step_ms) / 1e3) / 1e9 / hbm, 4)
+    if args.profile_json:
+        json.dump({"trace": trace, "records": recs, "step_ms": step_ms}, open(args.profile_json, "w"))
+    if args.dump_results:
+        json.dump({str(k): v for k, v in dump.items()}, open(args.dump_results.replace("{rank}", str(as_rank)), "w"))
 
     # gather counters over ranks (the only collective)
     allv = gather_counters([tokens, elapsed, e2e_tok, e2e_el],
-                           device="cpu" if os.environ.get("SV_DIST_BACKEND", "nccl") != "nccl" else "cuda")
+                           device="cpu" if backend not in (None, "nccl") else "cuda")
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -466,52 +628,20 @@ def run_ours(args):
     value = tot_tokens / t_max
     e2e_value = allv[:, 2].sum() / allv[:, 3].max()
 
-    # roofline of the dominant kernel family (the weight-streaming GEMM)
-    hbm, tc, peak_src = measured_peaks()
-    fam = {}
-    for r in recs:
-        k = r["kind"]
-        f = fam.setdefault(k, [0.0, 0.0, 0])
-        f[0] += r["bytes"]
-        f[1] += r["ms"]
-        f[2] += 1
-    dom_kinds = [k for k in fam if k.startswith("gemm")]
-    dom_name, tr_key = "gemm_kernel (QKV/O/gate-up/down/LM-head, tcgen05 + TMA)", "gemm"
-    g_bytes = sum(fam[k][0] for k in dom_kinds)
-    g_ms = sum(fam[k][1] for k in dom_kinds)
-    g_n = sum(fam[k][2] for k in dom_kinds)
-    step_ms_prof = sum(r["ms"] for r in recs)
-    achieved = g_bytes / (g_ms / 1e3) / 1e9
-    tr = ncu_traffic(tr_key)
-    step_bytes = sum(r["bytes"] for r in recs)
-    if exit_layers:   # the profiled step ran one exit; the timed steps ran len(exit_layers)
-        step_bytes += (len(exit_layers) - 1) * sum(r["bytes"] for r in recs
-                                                   if r["kind"] in ("gemm_lm_exit", "accept_exit"))
-    roofline = {"bound": "hbm", "kernel": dom_name,
-                "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                "traffic": tr, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": g_bytes / g_n, "avg_launch_ms": g_ms / g_n,
-                "share_of_step": round(g_ms / step_ms_prof, 4),
-                "step_algorithmic_bytes": step_bytes,
-                "step_frac_of_peak": round(step_bytes / (statistics.median(step_ms) / 1e3) / 1e9 / hbm, 4),
-                "kernels": {k: {"launches": v[2], "ms": round(v[1], 4), "GB/s": round(v[0] / (v[1] / 1e3) / 1e9, 1)}
-                            for k, v in fam.items()}}
-    if args.profile_json:
-        json.dump({"records": recs, "step_ms": step_ms}, open(args.profile_json, "w"))
-
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and not args.shard:
         _keep = _all_host_threads()
         sample = OracleSample(args, ctx)
-        t32, _ = sample.step()
-        cores, desc = host_cores(), sample.describe(t32)
+        dt, _ = sample.step()
         tps = expected_tau(gamma, args.alpha)
-        cpu = {"value": tps / t32, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": desc + f"; tokens/step {tps:.3f} = expected tau of the calibrated workload "
-                                f"(alpha {args.alpha}, gamma {gamma})"}
+        cpu = {"value": tps / dt, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
+               "sample": sample.describe() + f"; tokens/step {tps:.3f} = expected tau of the calibrated workload "
+                                             f"(alpha {args.alpha}, gamma {gamma})",
+               "host": host_identity()}
 
     h2d = per * gamma * mc.vocab * 4 + per * (gamma + 1) * 12   # gamma 0: no draft probabilities
     d2h = 2 * per * 64
+    tau_exp = expected_tau(gamma, args.alpha)
     line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_max * 1e3 / args.steps, 4),
             "latency_p50_ms": round(statistics.median(step_ms), 4),
@@ -528,12 +658,18 @@ def run_ours(args):
                        "exit_layer": exit_layers if exit_layers else exit_layer,
                        "engine": "per-op kernels + CUDA graph + PDL",
                        "parallelism": f"requests sharded over {world} GPU(s), weights replicated",
+                       "world_size": world, "dist_backend": backend,
+                       "draft_sets_per_request": n_sets,
                        "l2": "inputs larger than L2 (13.5 GB of weights streamed per step)"},
             "tokens_per_step": round(tot_tokens / (args.steps * total), 4),
+            "expected_tokens_per_step": round(tau_exp, 4),
+            "tokens_per_step_stderr": round(float(np.std(per_step_tok) / np.sqrt(len(per_step_tok) * per)), 4),
             "accepted_hist": accepted_hist.tolist(),
             "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": round(allv[:, 3].max() * 1e3 / args.steps, 4),
+                    "tokens_per_step": round(allv[:, 2].sum() / (args.steps * total), 4)},
             "gpu_launches": launches * args.steps, "kernels_per_step": launches,
+            "exit_ready": exit_ready,
             "prefill": ({"prompt_tokens": ctx, "ms_per_prompt_p50": round(1e3 * statistics.median(prefill_s), 3),
                          "tokens_per_s": round(ctx / statistics.median(prefill_s), 1),
                          "note": "sv_prefill, one synchronous call per request, host wall clock"}

@@ -41,7 +41,7 @@ extern "C" {
 #endif
 
 #define SV_MAX_GAMMA 8
-#define SV_ABI_VERSION 3
+#define SV_ABI_VERSION 4
 
 typedef enum {
     SV_OK = 0,
@@ -234,6 +234,21 @@ SV_API sv_status sv_wait_exit(sv_ticket* t, int32_t k, int64_t timeout_us);
 SV_API sv_status sv_exits_ready(sv_ticket* t, int32_t* n_ready);
 SV_API sv_status sv_ticket_release(sv_ticket* t);
 
+/* Exit-ready latency of a completed ticket (valid after sv_wait_final, before
+ * sv_ticket_release).  The paper's early exit exists to deliver a verified token
+ * mid-verification (Eq. 5; Alg-S lines 1103-1106).
+ *   exit_dev_ms [n_exits]: device time from the step's first kernel starting to the
+ *       last request of exit k having its result written (globaltimer, ns resolution);
+ *   final_dev_ms: the same for the final exit;
+ *   exit_host_ms [n_exits]: host time from the submit call to the first observation
+ *       (sv_wait_exit / sv_exits_ready / sv_wait_final) of exit k's mailbox flag;
+ *   final_host_ms: host time from the submit call to sv_wait_final observing the
+ *       step's completion.
+ * Any pointer may be NULL; a value is -1 when it was not observed (no GPU work,
+ * or the exit was never waited for).  Synchronous (one small device read). */
+SV_API sv_status sv_ticket_timing(sv_ticket* t, double* exit_dev_ms, double* final_dev_ms, double* exit_host_ms,
+                                  double* final_host_ms);
+
 /* Prefill: append the prompt tokens[0..n) to the
  * session's KV cache in one pass (positions len..len+n-1, causal inside the
  * prompt, Eq. 3) and emit the next token from the last prompt row:
@@ -279,6 +294,27 @@ typedef struct {
 SV_API sv_status sv_debug_profile_step(sv_engine* e, const sv_verify_req* reqs, int32_t n, int32_t exit_layer,
                                        sv_exit_result* early, sv_exit_result* final_, sv_kernel_prof* out,
                                        int32_t cap, int32_t* n_out);
+/* Non-committing forward: run tokens[0..n) as one block at
+ * positions len..len+n-1 of the session (causal inside the block, Eq. 3,
+ * PAPER.md:96-100) through every layer and the final head, and write the fp32
+ * logits of every row to logits_dev (device [n][vocab]).  The session is not
+ * changed: its length and round counter stay, the K/V rows the pass wrote beyond
+ * the cached length stay invisible.  Used for the GPU "KV-incremental == full
+ * recompute" pin.  n <= opts.max_prefill.  Synchronous. */
+SV_API sv_status sv_debug_forward(sv_session* s, const int32_t* tokens, int32_t n, float* logits_dev);
+/* Per-launch timeline of one step as it runs in production (graph replay with
+ * programmatic dependent launch): sv_debug_trace_next makes the next submit record,
+ * for every kernel launch, the globaltimer of its first CTA's start and its last
+ * CTA's end (a separately captured graph variant; untraced steps are unchanged).
+ * After sv_wait_final, sv_debug_trace_read copies up to cap records (host) in
+ * launch order; times are ns from the step's first kernel start; kind = SV_K_*,
+ * layer 0-based or -1, stream 0 = main, 1 = exit stream.  *n_out = records. */
+typedef struct {
+    int32_t kind, layer, stream, pad;
+    uint64_t start_ns, end_ns;
+} sv_trace_rec;
+SV_API sv_status sv_debug_trace_next(sv_engine* e);
+SV_API sv_status sv_debug_trace_read(sv_engine* e, sv_trace_rec* out, int32_t cap, int32_t* n_out);
 /* Philox4x32-10 evaluated on the device (host in/out).  Synchronous. */
 SV_API sv_status sv_debug_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 

@@ -31,7 +31,11 @@ __global__ void __launch_bounds__(ACC_THREADS) accept_kernel(const __grid_consta
     __shared__ AcceptSmem S;
     pdl_launch_dependents();
     pdl_wait();
-    accept_body<ACC_THREADS>(a, blockIdx.x, blockIdx.y, threadIdx.x, S, CtaSync{});
+    if (accept_body<ACC_THREADS>(a, blockIdx.x, blockIdx.y, threadIdx.x, S, CtaSync{}) && a.ready_stamp) {
+        unsigned long long t;   // exit-ready stamp: after this request's result is written
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t) :: "memory");
+        atomicMax(a.ready_stamp, t);
+    }
     __syncthreads();
     ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }

@@ -181,9 +181,14 @@ struct StepKey {
     int n, gamma;
     uint64_t exit_mask;   // bit l-1 set: early exit after decoder layer l
     int nchunk;
+    bool trace;           // per-launch timeline recorded (sv_debug_trace_next / SV_KTRACE)
     bool operator<(const StepKey& o) const {
-        return std::tie(n, gamma, exit_mask, nchunk) < std::tie(o.n, o.gamma, o.exit_mask, o.nchunk);
+        return std::tie(n, gamma, exit_mask, nchunk, trace) < std::tie(o.n, o.gamma, o.exit_mask, o.nchunk, o.trace);
     }
+};
+
+struct KMeta {
+    int kind, layer, stream;   // stream 0 = main, 1 = exit
 };
 
 struct sv_ticket {
@@ -203,6 +208,11 @@ struct sv_ticket {
     bool has_gpu;
     bool final_done = false;
     cudaEvent_t ev_done = nullptr;
+    // exit-ready timing (sv_ticket_timing): host clock at submit, at the first
+    // observation of each exit's mailbox flag and of the step's completion
+    std::chrono::steady_clock::time_point t_submit;
+    std::vector<double> exit_host_ms;
+    double final_host_ms = -1.0;
 };
 
 struct sv_engine {
@@ -236,6 +246,7 @@ struct sv_engine {
     int max_vreq = 1;                           // meta capacity: requests or prefill query blocks
     struct {                                    // set by sv_prefill for the duration of one issue_step
         bool on = false;
+        bool all_rows = false;                  // sv_debug_forward: LM head on every prompt row
         int n_tokens = 0, nq = 0, gb = 0;
     } pf;
     // device scratch
@@ -272,9 +283,16 @@ struct sv_engine {
     sv_ticket* inflight = nullptr;
     bool poisoned = false;
     std::vector<ProfRec>* prof = nullptr;
-    unsigned long long* ktrace = nullptr;       // SV_KTRACE: per-launch [start, ~end] globaltimer
-    std::vector<std::pair<int, int>> kmeta;     // (kind, layer) of each traced launch
+    unsigned long long* ktrace = nullptr;       // active trace buffer while a traced step is issued (else NULL)
+    unsigned long long* ktrace_buf = nullptr;   // per-launch [start, ~end] globaltimer, 1024 launches
+    bool trace_env = false;                     // SV_KTRACE: trace every step, CSV at sv_wait_final
+    bool trace_next = false;                    // sv_debug_trace_next: trace the next submit
+    bool trace_valid = false;                   // the last submit was traced
+    std::vector<KMeta> kmeta;                   // launches of the step being issued
+    std::map<StepKey, std::vector<KMeta>> graph_kmeta;
+    std::vector<KMeta> last_kmeta;              // launches of the last traced step
     unsigned long long* atrace = nullptr;       // SV_ATRACE: attention phase stamps [layer][16]
+    unsigned long long* stamps_dev = nullptr;   // [L+2] globaltimer: step start, exit k ready (1+k), final (1+L)
     std::mutex mu;
 };
 
@@ -289,6 +307,7 @@ static sv_status engine_alloc(sv_engine* e) {
         return r;
     };
     CK(dalloc((void**)&e->h, (size_t)MP * d * 4));
+    CK(dalloc((void**)&e->stamps_dev, (size_t)(e->L + 2) * 8));
     CK(dalloc((void**)&e->qbuf, (size_t)MP * d * 4));
     CK(dalloc((void**)&e->ssq, (size_t)(2 * e->L + 1) * (d / 128) * MP * 4));
     CK(dalloc((void**)&e->logits_exit, (size_t)MP * V * 4));
@@ -469,7 +488,8 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     CK(cudaStreamCreateWithFlags(&e->s_exit, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
-    if (getenv("SV_KTRACE")) CK(cudaMalloc((void**)&e->ktrace, 1024 * 2 * sizeof(unsigned long long)));
+    CK(cudaMalloc((void**)&e->ktrace_buf, 1024 * 2 * sizeof(unsigned long long)));
+    e->trace_env = getenv("SV_KTRACE") != nullptr;
     if (getenv("SV_ATRACE")) CK(cudaMalloc((void**)&e->atrace, (size_t)e->L * 16 * sizeof(unsigned long long)));
     *out = e;
     return SV_OK;
@@ -526,7 +546,7 @@ extern "C" sv_status sv_engine_destroy(sv_engine* e) {
                    e->attn_o, e->attn_ml, e->u, e->u_exit, e->attn_out, e->act, e->cnt_main, e->cnt_exit,
                    e->cnt_attn, e->cnt_acc_exit, e->cnt_acc_final, e->stats_exit, e->stats_final, e->race_exit,
                    e->race_final, e->res_exit_dev, e->res_final_dev, e->meta_dev, e->probs_stage,
-                   e->h_exit, e->ssq_ad, e->act_ad, e->u_ad};
+                   e->h_exit, e->ssq_ad, e->act_ad, e->u_ad, e->stamps_dev, e->ktrace_buf, e->atrace};
     for (void* p : dev)
         if (p) cudaFree(p);
     cudaFreeHost(e->meta_host);
@@ -665,18 +685,21 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         if ((r = (x)) != cudaSuccess) return r;         \
         if (e->ktrace) {                                \
             e->kmeta.resize(nl + 1);                    \
-            e->kmeta[nl] = {kind, layer};               \
+            e->kmeta[nl] = {kind, layer, s == st ? 0 : 1}; \
         }                                               \
         ++nl;                                           \
         pend(_a, kind, layer, s, bytes, flops);         \
     } while (0)
 
+    e->kmeta.clear();
     if (e->ktrace && (r = cudaMemsetAsync(e->ktrace, 0xFF, 1024 * 2 * sizeof(unsigned long long), st)) != cudaSuccess)
         return r;
     EmbedArgs ea{(const int32_t*)(e->meta_dev + e->off_tok), e->embed, e->norm_attn[0], e->h, e->u, ssq_at(e, 0, 0), M,
                  e->MP, d};
     ea.ktrace = e->ktrace;
     ea.ktrace_id = nl;
+    ea.stamps = e->stamps_dev;
+    ea.n_stamps = L + 2;
     LAUNCH(SV_K_EMBED, -1, st, Md * 2 + d * 2 + Md * 6 + (d / 128) * M * 4.0, 0.0, embed_launch(ea, st));
     double attn_bytes = Md * 6, attn_flops = 0;
     int max_ctx = 0;
@@ -743,11 +766,11 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         return gemm_launch(epi, tl, A, B, a, s);
     };
     // slot >= 0: the exit reads u_exit slot `slot`; slot < 0: the adapter output u_ad
-    auto lm_and_accept = [&](cudaStream_t s, bool is_exit, int exit_layer, int slot) -> cudaError_t {
-        GemmArgs a = base_args(e, pf ? 1 : M);
+    auto lm_and_accept = [&](cudaStream_t s, bool is_exit, int exit_layer, int slot, int stamp_slot) -> cudaError_t {
+        GemmArgs a = base_args(e, pf && !e->pf.all_rows ? 1 : M);
         a.ssq_in = (is_exit && slot < 0) ? e->ssq_ad : ssq_at(e, is_exit ? exit_layer : L, 0);
         a.b_row0 = (is_exit && slot >= 0) ? slot * e->MP : 0;
-        if (pf) {   // prefill: the LM head of the last prompt row only (its next token)
+        if (pf && !e->pf.all_rows) {   // prefill: the LM head of the last prompt row only (its next token)
             a.b_row0 = e->pf.n_tokens - 1;
             a.ssq_in += e->pf.n_tokens - 1;
         }
@@ -767,9 +790,15 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         aa.is_final = is_exit ? 0 : 1;
         aa.ktrace = e->ktrace;
         aa.ktrace_id = nl;
+        aa.ready_stamp = e->stamps_dev + stamp_slot;
         {
             cudaEvent_t _a = pbeg(s);
             if ((q = accept_launch(aa, s)) != cudaSuccess) return q;
+            if (e->ktrace) {   // one record [row_stats start, accept end] for the pair
+                e->kmeta.resize(nl + 2);
+                e->kmeta[nl] = {is_exit ? SV_K_ACCEPT_EXIT : SV_K_ACCEPT_FINAL, -1, s == st ? 0 : 1};
+                e->kmeta[nl + 1] = {-1, -1, -1};
+            }
             nl += 2;
             pend(_a, is_exit ? SV_K_ACCEPT_EXIT : SV_K_ACCEPT_FINAL, -1, s,
                  (double)M * V * 4 + (double)n * V * 8, 0.0);
@@ -862,8 +891,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
                 g2.ssq_out = e->ssq_ad;
                 LAUNCH(SV_K_LM_EXIT, l, e->s_exit, gemm_bytes(d, R, Md * 10), 2.0 * M * d * R,
                        gemm(EPI_RESID, 4 * L + 1 + L + l, 4, d, R, g2, e->s_exit, true));
-                if ((r = lm_and_accept(e->s_exit, true, l + 1, -1)) != cudaSuccess) return r;
-            } else if ((r = lm_and_accept(e->s_exit, true, l + 1, exit_k)) != cudaSuccess) {
+                if ((r = lm_and_accept(e->s_exit, true, l + 1, -1, 1 + exit_k)) != cudaSuccess) return r;
+            } else if ((r = lm_and_accept(e->s_exit, true, l + 1, exit_k, 1 + exit_k)) != cudaSuccess) {
                 return r;
             }
             if ((r = cudaMemcpyAsync(e->mb_exit + (size_t)exit_k * e->opts.max_batch, e->res_exit_dev,
@@ -877,7 +906,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             if (exit_k == n_exits && (r = cudaEventRecord(e->ev_join, e->s_exit)) != cudaSuccess) return r;
         }
     }
-    if ((r = lm_and_accept(st, false, L, 0)) != cudaSuccess) return r;
+    if ((r = lm_and_accept(st, false, L, 0, 1 + L)) != cudaSuccess) return r;
     if ((r = cudaMemcpyAsync(e->mb_final, e->res_final_dev, (size_t)n * sizeof(sv_exit_result), cudaMemcpyDeviceToHost,
                              st)) != cudaSuccess)
         return r;
@@ -891,26 +920,37 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
 static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, uint64_t exit_mask, int nchunk) {
     CK(cudaMemcpyAsync(e->meta_dev, e->meta_host, e->meta_bytes, cudaMemcpyHostToDevice, st));
     int nl = 0;
+    const bool trace = (e->trace_env || e->trace_next) && !e->prof;
+    e->trace_next = false;
+    e->trace_valid = trace;
+    e->ktrace = trace ? e->ktrace_buf : nullptr;
     if (!e->opts.use_graphs || e->prof) {
-        CK(issue_step(e, st, n, gamma, exit_mask, nchunk, &nl));
+        const cudaError_t r = issue_step(e, st, n, gamma, exit_mask, nchunk, &nl);
+        e->ktrace = nullptr;
+        CK(r);
         e->last_launches = nl;
+        if (trace) e->last_kmeta = e->kmeta;
         return SV_OK;
     }
-    StepKey key{n, gamma, exit_mask, nchunk};
+    StepKey key{n, gamma, exit_mask, nchunk, trace};
     auto it = e->graphs.find(key);
     if (it == e->graphs.end()) {
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(e->s_cap, cudaStreamCaptureModeThreadLocal));
         cudaError_t r = issue_step(e, e->s_cap, n, gamma, exit_mask, nchunk, &nl);
         cudaError_t r2 = cudaStreamEndCapture(e->s_cap, &g);
+        e->ktrace = nullptr;
         if (r != cudaSuccess) return fail(SV_E_DEVICE, std::string("capture: ") + cudaGetErrorString(r));
         CK(r2);
         cudaGraphExec_t ex;
         CK(cudaGraphInstantiate(&ex, g, 0));
         CK(cudaGraphDestroy(g));
         it = e->graphs.emplace(key, ex).first;
+        e->graph_kmeta[key] = e->kmeta;
         e->last_launches = nl;
     }
+    e->ktrace = nullptr;
+    if (trace) e->last_kmeta = e->graph_kmeta[key];
     CK(cudaGraphLaunch(it->second, st));
     return SV_OK;
 }
@@ -951,6 +991,8 @@ extern "C" sv_status sv_verify_submit_exits(sv_engine* e, const sv_verify_req* r
     cudaStream_t st = (cudaStream_t)stream;
     const int G = gamma + 1;
     sv_ticket* t = new sv_ticket();
+    t->t_submit = std::chrono::steady_clock::now();
+    t->exit_host_ms.assign(n_exits, -1.0);
     t->e = e; t->n = n; t->early = early; t->final_ = final_;
     t->exits.assign(exit_layers, exit_layers + n_exits);
     t->exit_done.assign(n_exits, false);
@@ -1050,6 +1092,68 @@ extern "C" sv_status sv_verify_submit(sv_engine* e, const sv_verify_req* reqs, i
     return sv_verify_submit_exits(e, reqs, n, &exit_layer, exit_layer > 0 ? 1 : 0, early, final_, stream, out);
 }
 
+static double ms_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+extern "C" sv_status sv_debug_trace_next(sv_engine* e) {
+    if (!e) return fail(SV_E_INVALID, "NULL engine");
+    std::lock_guard<std::mutex> lk(e->mu);
+    e->trace_next = true;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_debug_trace_read(sv_engine* e, sv_trace_rec* out, int32_t cap, int32_t* n_out) {
+    if (!e || !n_out || (cap > 0 && !out)) return fail(SV_E_INVALID, "NULL argument");
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (e->inflight) return fail(SV_E_BUSY, "a ticket is in flight");
+    if (!e->trace_valid) return fail(SV_E_INVALID, "the last submit was not traced");
+    const auto& km = e->last_kmeta;
+    std::vector<unsigned long long> tr(2 * km.size());
+    CK(cudaSetDevice(e->device));
+    CK(cudaMemcpy(tr.data(), e->ktrace_buf, tr.size() * 8, cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ull;
+    for (size_t i = 0; i < km.size(); ++i)
+        if (km[i].kind >= 0) t0 = std::min(t0, tr[2 * i]);
+    int k = 0;
+    for (size_t i = 0; i < km.size(); ++i) {
+        if (km[i].kind < 0) continue;
+        if (k < cap) {
+            sv_trace_rec& r = out[k];
+            r.kind = km[i].kind;
+            r.layer = km[i].layer;
+            r.stream = km[i].stream;
+            r.pad = 0;
+            r.start_ns = tr[2 * i] - t0;
+            r.end_ns = ~tr[2 * i + 1] - t0;
+        }
+        ++k;
+    }
+    *n_out = k;
+    return SV_OK;
+}
+
+extern "C" sv_status sv_ticket_timing(sv_ticket* t, double* exit_dev_ms, double* final_dev_ms, double* exit_host_ms,
+                                      double* final_host_ms) {
+    if (!t) return fail(SV_E_INVALID, "NULL ticket");
+    if (!t->final_done) return fail(SV_E_INVALID, "timing is available after sv_wait_final");
+    sv_engine* e = t->e;
+    const int ne = (int)t->exits.size();
+    std::vector<unsigned long long> st(e->L + 2, 0);
+    if (t->has_gpu) {
+        CK(cudaSetDevice(e->device));
+        CK(cudaMemcpy(st.data(), e->stamps_dev, st.size() * 8, cudaMemcpyDeviceToHost));
+    }
+    auto dev = [&](int slot) { return (t->has_gpu && st[slot] >= st[0] && st[0]) ? (st[slot] - st[0]) * 1e-6 : -1.0; };
+    for (int k = 0; k < ne; ++k) {
+        if (exit_dev_ms) exit_dev_ms[k] = dev(1 + k);
+        if (exit_host_ms) exit_host_ms[k] = t->exit_host_ms[k];
+    }
+    if (final_dev_ms) *final_dev_ms = dev(1 + e->L);
+    if (final_host_ms) *final_host_ms = t->final_host_ms;
+    return SV_OK;
+}
+
 static void fill_host_result(sv_exit_result* r, const sv_ticket* t, int i, int exit_layer, int is_final) {
     memset(r, 0, sizeof(*r));
     r->round_id = t->rounds[i];
@@ -1081,6 +1185,7 @@ extern "C" sv_status sv_wait_exit(sv_ticket* t, int32_t k, int64_t timeout_us) {
             std::this_thread::yield();
         }
     }
+    if (t->exit_host_ms[k] < 0) t->exit_host_ms[k] = ms_since(t->t_submit);
     const sv_exit_result* row = e->mb_exit + (size_t)k * e->opts.max_batch;
     for (int i = 0; i < t->n; ++i) {
         sv_exit_result* dst = t->early + (size_t)k * t->n + i;
@@ -1101,7 +1206,10 @@ extern "C" sv_status sv_exits_ready(sv_ticket* t, int32_t* n_ready) {
         return fail(SV_E_DEVICE, std::string("step failed: ") + cudaGetErrorString(q));
     }
     const bool all = q == cudaSuccess;
-    while (k < (int)t->exits.size() && (all || e->mb_flag[k] == t->seq)) ++k;
+    while (k < (int)t->exits.size() && (all || e->mb_flag[k] == t->seq)) {
+        if (t->exit_host_ms[k] < 0) t->exit_host_ms[k] = ms_since(t->t_submit);
+        ++k;
+    }
     *n_ready = k;
     return SV_OK;
 }
@@ -1122,7 +1230,10 @@ extern "C" sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us) {
     const auto t0 = std::chrono::steady_clock::now();
     for (;;) {
         cudaError_t q = cudaEventQuery(t->ev_done);
-        if (q == cudaSuccess) break;
+        if (q == cudaSuccess) {
+            if (t->final_host_ms < 0) t->final_host_ms = ms_since(t->t_submit);
+            break;
+        }
         if (q != cudaErrorNotReady) {
             e->poisoned = true;
             return fail(SV_E_DEVICE, std::string("step failed: ") + cudaGetErrorString(q));
@@ -1150,14 +1261,14 @@ extern "C" sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us) {
         }
     }
     t->final_done = true;
-    if (e->ktrace && getenv("SV_KTRACE")) {   // per-launch timeline of this step
-        std::vector<unsigned long long> tr(2 * e->kmeta.size());
-        if (cudaMemcpy(tr.data(), e->ktrace, tr.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
+    if (e->trace_valid && e->trace_env) {   // per-launch timeline of this step (SV_KTRACE=<csv>)
+        std::vector<unsigned long long> tr(2 * e->last_kmeta.size());
+        if (cudaMemcpy(tr.data(), e->ktrace_buf, tr.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
             FILE* fp = fopen(getenv("SV_KTRACE"), "w");
             if (fp) {
                 fprintf(fp, "id,kind,layer,start_ns,end_ns\n");
-                for (size_t i = 0; i < e->kmeta.size(); ++i)
-                    fprintf(fp, "%zu,%d,%d,%llu,%llu\n", i, e->kmeta[i].first, e->kmeta[i].second, tr[2 * i],
+                for (size_t i = 0; i < e->last_kmeta.size(); ++i)
+                    fprintf(fp, "%zu,%d,%d,%llu,%llu\n", i, e->last_kmeta[i].kind, e->last_kmeta[i].layer, tr[2 * i],
                             ~tr[2 * i + 1]);
                 fclose(fp);
             }
@@ -1196,8 +1307,8 @@ extern "C" sv_status sv_ticket_release(sv_ticket* t) {
 // over the shared page table, causal inside the prompt) and emit the next token
 // from the last row (argmax, or a race sample of p with the session's Philox
 // stream at round_id = last_round + 1).  Synchronous, no CUDA graph.
-extern "C" sv_status sv_prefill(sv_session* s, const int32_t* tokens, int32_t n, int32_t sample,
-                                sv_exit_result* out) {
+static sv_status prefill_pass(sv_session* s, const int32_t* tokens, int32_t n, int32_t sample, sv_exit_result* out,
+                              float* logits_dev) {
     if (!s || !tokens || !out || n < 1) return fail(SV_E_INVALID, "bad arguments");
     sv_engine* e = s->e;
     std::lock_guard<std::mutex> lk(e->mu);
@@ -1240,6 +1351,7 @@ extern "C" sv_status sv_prefill(sv_session* s, const int32_t* tokens, int32_t n,
     cudaStream_t st = e->s_cap;
     CK(cudaMemcpyAsync(e->meta_dev, e->meta_host, e->meta_bytes, cudaMemcpyHostToDevice, st));
     e->pf.on = true;
+    e->pf.all_rows = logits_dev != nullptr;
     e->pf.n_tokens = n;
     e->pf.nq = nq;
     e->pf.gb = gb;
@@ -1247,19 +1359,34 @@ extern "C" sv_status sv_prefill(sv_session* s, const int32_t* tokens, int32_t n,
     const int nchunk = std::min(e->max_nchunk, (len + n + 63) / 64);
     cudaError_t r = issue_step(e, st, 1, 0, 0ull, nchunk, &nl);
     e->pf.on = false;
+    e->pf.all_rows = false;
     if (r == cudaSuccess) r = cudaMemcpyAsync(out, e->res_final_dev, sizeof(sv_exit_result), cudaMemcpyDeviceToHost, st);
+    if (r == cudaSuccess && logits_dev)
+        r = cudaMemcpyAsync(logits_dev, e->logits_final, (size_t)n * e->V * 4, cudaMemcpyDeviceToDevice, st);
     if (r == cudaSuccess) r = cudaStreamSynchronize(st);
     if (r != cudaSuccess) {
         e->poisoned = true;
         return fail(SV_E_DEVICE, std::string("prefill: ") + cudaGetErrorString(r));
     }
     e->last_launches = nl;
+    if (logits_dev) return SV_OK;   // non-committing: the written rows stay invisible
     if (out->status == SV_OK) {
         s->len = len + n;
         s->last_round = out->round_id;
         out->new_len = s->len;
     }
     return (sv_status)out->status;
+}
+
+extern "C" sv_status sv_prefill(sv_session* s, const int32_t* tokens, int32_t n, int32_t sample,
+                                sv_exit_result* out) {
+    return prefill_pass(s, tokens, n, sample, out, nullptr);
+}
+
+extern "C" sv_status sv_debug_forward(sv_session* s, const int32_t* tokens, int32_t n, float* logits_dev) {
+    if (!logits_dev) return fail(SV_E_INVALID, "NULL logits");
+    sv_exit_result r;
+    return prefill_pass(s, tokens, n, 0, &r, logits_dev);
 }
 
 extern "C" sv_status sv_verify(sv_session* s, const sv_verify_req* req, int32_t exit_layer, sv_exit_result* early,
@@ -1388,14 +1515,11 @@ extern "C" sv_status sv_debug_profile_step(sv_engine* e, const sv_verify_req* re
     e->prof = &recs;
     const bool pdl = g_use_pdl;
     g_use_pdl = false;   // serialise kernels so events bracket exactly one launch
-    unsigned long long* kt = e->ktrace;
-    e->ktrace = nullptr;  // the SV_KTRACE timeline records graph replays only
     sv_ticket* t = nullptr;
     sv_status s = sv_verify_submit(e, reqs, n, exit_layer, early, final_, nullptr, &t);
     e->prof = nullptr;
     g_use_pdl = pdl;
     if (!s) s = sv_ticket_release(t);
-    e->ktrace = kt;
     if (s) return s;
     CK(cudaDeviceSynchronize());
     int k = 0;

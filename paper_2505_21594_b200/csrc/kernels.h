@@ -142,6 +142,7 @@ struct AcceptArgs {
     int exit_layer, is_final;
     unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
     int ktrace_id = 0;
+    unsigned long long* ready_stamp = nullptr;   // globaltimer when the last request's result was written (max)
 };
 cudaError_t accept_launch(const AcceptArgs& a, cudaStream_t st);
 int accept_chunks(int V, int* chunk);
@@ -157,6 +158,8 @@ struct EmbedArgs {
     int M, MP, d;
     unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
     int ktrace_id = 0;
+    unsigned long long* stamps = nullptr;   // [n_stamps]: [0] = step start (globaltimer), rest reset to 0
+    int n_stamps = 0;
 };
 cudaError_t embed_launch(const EmbedArgs& a, cudaStream_t st);
 

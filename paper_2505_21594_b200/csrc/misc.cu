@@ -17,6 +17,11 @@ __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ Embe
     pdl_launch_dependents();
     pdl_wait();
     const int m = blockIdx.x, t = blockIdx.y;
+    if (a.stamps && m == 0 && t == 0 && threadIdx.x < a.n_stamps) {   // step start; ready stamps reset
+        unsigned long long now = 0;                                    // (every reader is downstream)
+        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+        a.stamps[threadIdx.x] = now;
+    }
     const int k = t * 128 + threadIdx.x;
     const int tok = a.tok[m];
     const float hv = __bfloat162float(reinterpret_cast<const bf16*>(a.embed)[(size_t)tok * a.d + k]);

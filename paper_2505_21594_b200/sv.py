@@ -76,6 +76,11 @@ class sv_kernel_prof(C.Structure):
                 ("flops", C.c_double)]
 
 
+class sv_trace_rec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("layer", C.c_int32), ("stream", C.c_int32), ("pad", C.c_int32),
+                ("start_ns", C.c_uint64), ("end_ns", C.c_uint64)]
+
+
 KERNEL_KINDS = ["embed", "gemm_qkv", "attention", "gemm_o", "gemm_gate_up", "gemm_down",
                 "gemm_lm_exit", "accept_exit", "gemm_lm_final", "accept_final"]
 
@@ -114,12 +119,17 @@ EXPORTS = {
     "sv_wait_early": (C.c_int, [C.c_void_p, C.c_int64]),
     "sv_wait_final": (C.c_int, [C.c_void_p, C.c_int64]),
     "sv_ticket_release": (C.c_int, [C.c_void_p]),
+    "sv_ticket_timing": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "sv_verify": (C.c_int, [C.c_void_p, C.POINTER(sv_verify_req), C.c_int32, C.POINTER(sv_exit_result),
                             C.POINTER(sv_exit_result)]),
     "sv_debug_logits": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "sv_debug_accept": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(sv_verify_req), C.c_int32,
                                   C.POINTER(sv_exit_result)]),
     "sv_debug_kv_rows": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "sv_debug_trace_next": (C.c_int, [C.c_void_p]),
+    "sv_debug_trace_read": (C.c_int, [C.c_void_p, C.POINTER(sv_trace_rec), C.c_int32, C.POINTER(C.c_int32)]),
+    "sv_debug_forward": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_void_p]),
     "sv_debug_philox": (C.c_int, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
 }
 
@@ -282,6 +292,16 @@ class Session:
         self.last_round = out.round_id
         return out
 
+    def debug_forward(self, tokens):
+        """fp32 logits [n, V] (torch, on the engine's device) of tokens as one block after
+        the cached context, without committing anything (sv_debug_forward)."""
+        import torch
+        t = np.ascontiguousarray(np.asarray(tokens, dtype=np.int32))
+        out = torch.empty((len(t), self.engine.mc.vocab), dtype=torch.float32, device=f"cuda:{self.engine.device}")
+        check(lib().sv_debug_forward(self.h, t.ctypes.data_as(C.POINTER(C.c_int32)), len(t),
+                                     C.c_void_p(out.data_ptr())))
+        return out
+
     def close(self):
         if self.h:
             check(lib().sv_session_close(self.h))
@@ -354,6 +374,26 @@ class Ticket:
                           device=f"cuda:{self.engine.device}")
         check(lib().sv_debug_logits(self.h, which, C.c_void_p(out.data_ptr())))
         return out
+
+    def timing(self):
+        """Exit-ready latency after wait_final: dict(exit_dev_ms [n_exits], final_dev_ms,
+        exit_host_ms [n_exits], final_host_ms) (include/sv.h sv_ticket_timing)."""
+        ne = max(1, len(self.exit_layers))
+        ed, eh = (C.c_double * ne)(), (C.c_double * ne)()
+        fd, fh = C.c_double(), C.c_double()
+        check(lib().sv_ticket_timing(self.h, ed, C.byref(fd), eh, C.byref(fh)))
+        k = len(self.exit_layers)
+        return dict(exit_dev_ms=list(ed)[:k], final_dev_ms=fd.value, exit_host_ms=list(eh)[:k],
+                    final_host_ms=fh.value)
+
+    def final_ready(self) -> bool:
+        """Non-blocking: whether the final result has completed (sv_wait_final with a
+        zero timeout; it consumes the results if so)."""
+        s = lib().sv_wait_final(self.h, 0)
+        if s == SV_E_TIMEOUT:
+            return False
+        check(s)
+        return True
 
     def release(self):
         if self.h:
@@ -434,6 +474,18 @@ class Engine:
         recs = [dict(kind=KERNEL_KINDS[out[i].kind], layer=out[i].layer, ms=out[i].ms, bytes=out[i].bytes,
                      flops=out[i].flops) for i in range(min(k.value, cap))]
         return [final[i] for i in range(n)], recs
+
+    def trace_next(self):
+        """Record a per-launch timeline of the next submit (graph replay, PDL on)."""
+        check(lib().sv_debug_trace_next(self.h))
+
+    def trace_read(self, cap: int = 2048):
+        """Timeline of the last traced step: list of dict(kind, layer, stream, start_us, end_us)."""
+        out = (sv_trace_rec * cap)()
+        k = C.c_int32()
+        check(lib().sv_debug_trace_read(self.h, out, cap, C.byref(k)))
+        return [dict(kind=KERNEL_KINDS[out[i].kind], layer=out[i].layer, stream=out[i].stream,
+                     start_us=out[i].start_ns / 1e3, end_us=out[i].end_ns / 1e3) for i in range(min(k.value, cap))]
 
     def set_adapters(self, adapters):
         """Exit adapters for every early exit (None: the plain shared head)."""
