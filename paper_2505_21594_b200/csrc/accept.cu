@@ -6,11 +6,14 @@
 namespace sv {
 
 constexpr int ACC_THREADS = 256;
-constexpr int ACC_CHUNK = 4096;
+constexpr int ACC_CHUNK = 1024;   // 32 CTAs per request at V = 32000: the race is ALU-latency bound
 
+// vocabulary chunks of ACC_CHUNK (a multiple of it for V > 32 * ACC_CHUNK): at most
+// 32 chunks, so a warp merges a row's chunk statistics / race parts in one step
 int accept_chunks(int V, int* chunk) {
-    *chunk = ACC_CHUNK;
-    return (V + ACC_CHUNK - 1) / ACC_CHUNK;
+    const int mult = (V + 32 * ACC_CHUNK - 1) / (32 * ACC_CHUNK);
+    *chunk = ACC_CHUNK * (mult > 0 ? mult : 1);
+    return (V + *chunk - 1) / *chunk;
 }
 
 struct CtaSync {
@@ -23,20 +26,29 @@ __global__ void __launch_bounds__(ACC_THREADS) row_stats_kernel(const __grid_con
     pdl_wait();
     const int row = blockIdx.x;
     ktrace_mark(a.ktrace, a.ktrace_id, 0);
+    unsigned long long* gtr = threadIdx.x == 0 ? a.gtrace : nullptr;
+    gphase_mark(gtr, a.ktrace_id + 1, 1);
     if (a.req[row / a.G].status_in != 0) return;
     row_stats_body<ACC_THREADS>(a, row, blockIdx.y, threadIdx.x, S, CtaSync{});
+    gphase_mark(gtr, a.ktrace_id + 1, 5);
 }
 
 __global__ void __launch_bounds__(ACC_THREADS) accept_kernel(const __grid_constant__ AcceptArgs a) {
     __shared__ AcceptSmem S;
     pdl_launch_dependents();
+    unsigned long long* gtr = threadIdx.x == 0 ? a.gtrace : nullptr;
+    gphase_mark(gtr, a.ktrace_id, 0);
+    accept_pre<ACC_THREADS>(a, blockIdx.x, blockIdx.y, threadIdx.x, S);
     pdl_wait();
+    gphase_mark(gtr, a.ktrace_id, 1);
     if (accept_body<ACC_THREADS>(a, blockIdx.x, blockIdx.y, threadIdx.x, S, CtaSync{}) && a.ready_stamp) {
         unsigned long long t;   // exit-ready stamp: after this request's result is written
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t) :: "memory");
         atomicMax(a.ready_stamp, t);
+        gphase_mark(a.gtrace, a.ktrace_id, 6);
     }
     __syncthreads();
+    gphase_mark(gtr, a.ktrace_id, 5);
     ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 

@@ -93,6 +93,7 @@ __device__ __forceinline__ Race race_shfl(const Race& s, int o) {
 struct AcceptSmem {
     float sM[SV_MAX_GAMMA + 1], sSum[SV_MAX_GAMMA + 1], sM2[SV_MAX_GAMMA + 1];
     int sA[SV_MAX_GAMMA + 1];
+    float sQx[SV_MAX_GAMMA], sU[SV_MAX_GAMMA], sRatio[SV_MAX_GAMMA];   // per drafted position
     int s_delta, s_status, s_last;
     float s_margin;
     Stat wst[8];
@@ -107,12 +108,31 @@ __device__ void row_stats_body(const AcceptArgs& a, int row, int c, int tid, Acc
     const float* z = a.logits + (size_t)row * a.V;
     const int v0 = c * a.chunk, v1 = min(a.V, v0 + a.chunk);
     Stat s{-INFINITY, -INFINITY, 0.f, INT_MAX};
-    for (int v = v0 + tid * 4; v < v1; v += NT * 4) {
-        const float4 x = __ldcg(reinterpret_cast<const float4*>(z + v));
-        stat_push(s, x.x, v);
-        stat_push(s, x.y, v + 1);
-        stat_push(s, x.z, v + 2);
-        stat_push(s, x.w, v + 3);
+    // every load of the thread's share in flight before the first use (one L2 round
+    // trip instead of one per iteration; the chunk is <= 4 float4 per thread)
+    constexpr int PER = 4;
+    float4 x[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int v = v0 + (tid + k * NT) * 4;
+        x[k] = v < v1 ? __ldcg(reinterpret_cast<const float4*>(z + v)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int v = v0 + (tid + k * NT) * 4;
+        if (v < v1) {
+            stat_push(s, x[k].x, v);
+            stat_push(s, x[k].y, v + 1);
+            stat_push(s, x[k].z, v + 2);
+            stat_push(s, x[k].w, v + 3);
+        }
+    }
+    for (int v = v0 + (tid + PER * NT) * 4; v < v1; v += NT * 4) {   // chunks beyond PER * NT * 4
+        const float4 y = __ldcg(reinterpret_cast<const float4*>(z + v));
+        stat_push(s, y.x, v);
+        stat_push(s, y.y, v + 1);
+        stat_push(s, y.z, v + 2);
+        stat_push(s, y.w, v + 3);
     }
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) s = stat_merge(s, stat_shfl(s, o));
@@ -126,8 +146,30 @@ __device__ void row_stats_body(const AcceptArgs& a, int row, int c, int tid, Acc
     sync();
 }
 
-// Acceptance for request b, vocabulary chunk c.  Returns true in exactly one
-// thread (the one that wrote a.out[b]) over all chunks of the request.
+// The acceptance inputs that do not depend on this step's logits, fetched before
+// griddepcontrol.wait (they overlap the LM head): q_j(x_j) and the acceptance
+// uniform u_j of every drafted position (one thread each, in parallel), and the
+// draft rows the race may read -> L2.
+template <int NT>
+__device__ void accept_pre(const AcceptArgs& a, int b, int c, int tid, AcceptSmem& S) {
+    const ReqDev& rq = a.req[b];
+    const int gamma = a.G - 1;
+    const float* q = reinterpret_cast<const float*>(rq.probs);
+    if (rq.status_in != 0 || q == nullptr) return;
+    if (tid < gamma) {
+        S.sQx[tid] = q[(size_t)tid * a.V + rq.drafts[tid]];
+        const u32x4 w = philox4x32_10(u32x4{0u, (uint32_t)tid, rq.round_id, rq.session_id},
+                                      (uint32_t)rq.philox_seed, (uint32_t)(rq.philox_seed >> 32));
+        S.sU[tid] = u32_to_uniform(w.x);
+    }
+    if (tid >= 32 && tid < 32 + gamma) {   // this CTA's vocabulary chunk of every draft row
+        const int v0 = c * a.chunk, n = min(a.V, v0 + a.chunk) - v0;
+        bulk_prefetch_l2(q + (size_t)(tid - 32) * a.V + v0, (uint32_t)(n * 4) & ~15u);
+    }
+}
+
+// Acceptance for request b, vocabulary chunk c (accept_pre has run).  Returns
+// true in exactly one thread (the one that wrote a.out[b]) over all chunks.
 template <int NT, class Sync>
 __device__ bool accept_body(const AcceptArgs& a, int b, int c, int tid, AcceptSmem& S, Sync sync) {
     const int G = a.G, gamma = G - 1, V = a.V;
@@ -145,16 +187,29 @@ __device__ bool accept_body(const AcceptArgs& a, int b, int c, int tid, AcceptSm
     const bool greedy = (q == nullptr);
     if (greedy && c != 0) return false;   // greedy needs no race
 
-    // merge row statistics in chunk order (identical in every CTA of the request)
-    if (tid < G) {
-        const float4* st = reinterpret_cast<const float4*>(a.stats + (size_t)(b * G + tid) * a.nch);
-        float4 s0 = __ldcg(&st[0]);
-        Stat t{s0.x, s0.y, s0.z, __float_as_int(s0.w)};
-        for (int k = 1; k < a.nch; ++k) {
-            const float4 sk = __ldcg(&st[k]);
-            t = stat_merge(t, Stat{sk.x, sk.y, sk.z, __float_as_int(sk.w)});
+    // merge the row statistics of the vocabulary chunks: warp w takes rows w, w+8, ..,
+    // lane k loads chunk k (nch <= 32, all in flight at once), a fixed butterfly tree
+    // merges them (identical in every CTA of the request: deterministic)
+    for (int row = tid >> 5; row < G; row += NT / 32) {
+        const int k = tid & 31;
+        Stat t{-INFINITY, -INFINITY, 0.f, INT_MAX};
+        if (k < a.nch) {
+            const float4 s4 = __ldcg(reinterpret_cast<const float4*>(a.stats + (size_t)(b * G + row) * a.nch) + k);
+            t = Stat{s4.x, s4.y, s4.z, __float_as_int(s4.w)};
         }
-        S.sM[tid] = t.m1; S.sM2[tid] = t.m2; S.sSum[tid] = t.sum; S.sA[tid] = t.idx;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) t = stat_merge(t, stat_shfl(t, o));
+        if (k == 0) {
+            S.sM[row] = t.m1; S.sM2[row] = t.m2; S.sSum[row] = t.sum; S.sA[row] = t.idx;
+        }
+    }
+    sync();
+    gphase_mark(tid == 0 ? a.gtrace : nullptr, a.ktrace_id, 2);
+    if (!greedy && tid < gamma) {   // p_{j-1}(x_j) / q_j(x_j) of every position at once
+        const int x = rq.drafts[tid];
+        const float zx = __ldcg(&a.logits[(size_t)(b * G + tid) * V + x]);
+        const float p = expf(zx - S.sM[tid]) / S.sSum[tid];
+        S.sRatio[tid] = p / S.sQx[tid];
     }
     sync();
     if (tid == 0) {
@@ -169,16 +224,11 @@ __device__ bool accept_body(const AcceptArgs& a, int b, int c, int tid, AcceptSm
             if (delta == gamma) margin = fminf(margin, S.sM[gamma] - S.sM2[gamma]);
         } else {
             for (int j = 1; j <= gamma; ++j)
-                if (!(q[(size_t)(j - 1) * V + rq.drafts[j - 1]] > 0.f)) status = SV_E_PROTOCOL;
+                if (!(S.sQx[j - 1] > 0.f)) status = SV_E_PROTOCOL;
             if (status == SV_OK) {
                 for (int j = 1; j <= gamma; ++j) {
-                    const int x = rq.drafts[j - 1];
-                    const float zx = __ldcg(&a.logits[(size_t)(b * G + j - 1) * V + x]);
-                    const float p = expf(zx - S.sM[j - 1]) / S.sSum[j - 1];
-                    const float ratio = p / q[(size_t)(j - 1) * V + x];
-                    const u32x4 w = philox4x32_10(u32x4{0u, (uint32_t)(j - 1), rq.round_id, rq.session_id},
-                                                  (uint32_t)rq.philox_seed, (uint32_t)(rq.philox_seed >> 32));
-                    const float u = u32_to_uniform(w.x);
+                    const float ratio = S.sRatio[j - 1];
+                    const float u = S.sU[j - 1];
                     margin = fminf(margin, fabsf(u - ratio));
                     if (!(u < ratio)) break;
                     delta = j;
@@ -186,6 +236,7 @@ __device__ bool accept_body(const AcceptArgs& a, int b, int c, int tid, AcceptSm
             }
         }
         S.s_delta = delta; S.s_status = status; S.s_margin = margin;
+        gphase_mark(a.gtrace, a.ktrace_id, 3);
     }
     sync();
     const int delta = S.s_delta;
@@ -201,15 +252,21 @@ __device__ bool accept_body(const AcceptArgs& a, int b, int c, int tid, AcceptSm
         const int v0 = c * a.chunk, v1 = min(V, v0 + a.chunk);
         const uint32_t c1 = (uint32_t)delta | (1u << 8);
         Race rc{0.f, 0.f, 0.f, INT_MAX, INT_MAX};
-        for (int v = v0 + tid * 4; v < v1; v += NT * 4) {
+        // loads of the thread's share first (one round trip), then the race
+        constexpr int PER = 4;
+        float4 zz[PER], qq[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int v = v0 + (tid + k * NT) * 4;
+            zz[k] = v < v1 ? __ldcg(reinterpret_cast<const float4*>(z + v)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            qq[k] = (qr && v < v1) ? __ldg(reinterpret_cast<const float4*>(qr + v)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        auto push4 = [&](int v, const float4& z4, const float4& q4) {
             const u32x4 w = philox4x32_10(u32x4{(uint32_t)(v >> 2), c1, rq.round_id, rq.session_id},
                                           (uint32_t)rq.philox_seed, (uint32_t)(rq.philox_seed >> 32));
             const uint32_t words[4] = {w.x, w.y, w.z, w.w};
-            const float4 zz = __ldcg(reinterpret_cast<const float4*>(z + v));
-            const float zs[4] = {zz.x, zz.y, zz.z, zz.w};
-            float4 qq = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (qr) qq = __ldg(reinterpret_cast<const float4*>(qr + v));
-            const float qs[4] = {qq.x, qq.y, qq.z, qq.w};
+            const float zs[4] = {z4.x, z4.y, z4.z, z4.w};
+            const float qs[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const float p = expf(zs[t] - M) * inv_s;
@@ -217,6 +274,16 @@ __device__ bool accept_body(const AcceptArgs& a, int b, int c, int tid, AcceptSm
                 const float E = -logf(u32_to_uniform(words[t]));
                 race_push(rc, wv / E, p / E, v + t);
             }
+        };
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int v = v0 + (tid + k * NT) * 4;
+            if (v < v1) push4(v, zz[k], qq[k]);
+        }
+        for (int v = v0 + (tid + PER * NT) * 4; v < v1; v += NT * 4) {   // beyond PER * NT * 4
+            const float4 z4 = __ldcg(reinterpret_cast<const float4*>(z + v));
+            const float4 q4 = qr ? __ldg(reinterpret_cast<const float4*>(qr + v)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            push4(v, z4, q4);
         }
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) rc = race_merge(rc, race_shfl(rc, o));
@@ -227,14 +294,20 @@ __device__ bool accept_body(const AcceptArgs& a, int b, int c, int tid, AcceptSm
             for (int w = 1; w < NT / 32; ++w) t = race_merge(t, S.wrc[w]);
             a.race[(size_t)b * a.nch + c] = RacePart{t.k1, t.k2, t.f1, t.v1, t.fv1, {0, 0, 0}};
             S.s_last = (atomic_add_acq_rel(&a.counters[b], 1) == a.nch - 1);
+            gphase_mark(a.gtrace, a.ktrace_id, 4);
         }
         sync();
-        if (!S.s_last || tid != 0) return false;
+        if (!S.s_last || tid >= 32) return false;
+        // the last CTA merges every chunk's race part: lane k loads part k (nch <= 32);
+        // race_merge is associative and commutative (max key, lowest index on ties)
         const RacePart* rp = a.race + (size_t)b * a.nch;
-        Race t{__ldcg(&rp[0].k1), __ldcg(&rp[0].k2), __ldcg(&rp[0].f1), __ldcg(&rp[0].v1), __ldcg(&rp[0].fv1)};
-        for (int k = 1; k < a.nch; ++k)
-            t = race_merge(t, Race{__ldcg(&rp[k].k1), __ldcg(&rp[k].k2), __ldcg(&rp[k].f1), __ldcg(&rp[k].v1),
-                                   __ldcg(&rp[k].fv1)});
+        Race t{0.f, 0.f, 0.f, INT_MAX, INT_MAX};
+        if (tid < a.nch)
+            t = Race{__ldcg(&rp[tid].k1), __ldcg(&rp[tid].k2), __ldcg(&rp[tid].f1), __ldcg(&rp[tid].v1),
+                     __ldcg(&rp[tid].fv1)};
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) t = race_merge(t, race_shfl(t, o));
+        if (tid != 0) return false;
         a.counters[b] = 0;
         if (t.k1 > 0.f) {
             next = t.v1;

@@ -157,8 +157,10 @@ __global__ void __launch_bounds__(128, MINB) attn3_kernel(const __grid_constant_
         issue(warp + A3_WARPS * pre, pre);
         ++pre;
     }
+    if (tid == 32 && a.pf_ptr && a.pf_early)   // O weights -> L2 while the QKV grid drains
+        cta_prefetch_l2(a.pf_ptr, a.pf_bytes, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y);
     pdl_wait();
-    if (tid == 32 && a.pf_ptr)   // the QKV GEMM is done: pull the O weights into L2 while HBM is idle
+    if (tid == 32 && a.pf_ptr && !a.pf_early)   // the QKV GEMM is done: pull the O weights into L2 while HBM is idle
         cta_prefetch_l2(a.pf_ptr, a.pf_bytes, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y);
     A3_STAMP(2);
     for (int it = pre; it < NST && it < n_my; ++it) issue(warp + A3_WARPS * it, it);

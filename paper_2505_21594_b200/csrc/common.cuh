@@ -180,6 +180,17 @@ __device__ __forceinline__ void ktrace_mark(unsigned long long* tr, int id, int 
     }
 }
 
+// phase stamps of a GEMM launch over all CTAs (SV_GTRACE): slot (id, phase) holds
+// [earliest, ~latest] globaltimer (buffer initialised to ~0)
+__device__ __forceinline__ void gphase_mark(unsigned long long* tr, int id, int phase) {
+    if (tr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        atomicMin(&tr[(id * 16 + phase) * 2], t);
+        atomicMin(&tr[(id * 16 + phase) * 2 + 1], ~t);
+    }
+}
+
 // ticket for "the last CTA to arrive does the merge": one acq_rel atomic by the
 // calling thread (release: its prior writes and, after a CTA barrier, the CTA's;
 // acquire: the other arrivals' writes for the merge that follows)

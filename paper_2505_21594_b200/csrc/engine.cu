@@ -223,7 +223,9 @@ struct sv_engine {
     bool no_box = false;                        // env SV_NO_BOX: load full token tiles
     bool no_t160 = false;                       // env SV_NO_T160: no 160-token persistent tiles
     bool no_wave = false;                       // env SV_NO_WAVE: always 256-token tiles above 128 rows
-    bool attn_pf = false;                       // attention prefetches the O weights to L2 (env SV_ATTN_PF; measured slower)
+    bool no_warm = false;                       // env SV_NO_WARM: no instruction-cache warm-up pass in gemm_kernel
+    int attn_pf = 0;                            // attention prefetches the O weights to L2 (env SV_ATTN_PF=1 after
+                                                // griddepcontrol.wait, 2 before it)
     int attn_splits = 0;                        // attention split override (env SV_ATTN_SPLITS; 0 = attn3_splits)
     std::vector<CUtensorMap> wmap128;           // weight maps [qkv L][o L][gu L][down L][lm] (box rows 128)
     // exit adapters (NEXT-3): weights, maps [dn L][up L], exit-stream buffers
@@ -285,6 +287,7 @@ struct sv_engine {
     std::vector<ProfRec>* prof = nullptr;
     unsigned long long* ktrace = nullptr;       // active trace buffer while a traced step is issued (else NULL)
     unsigned long long* ktrace_buf = nullptr;   // per-launch [start, ~end] globaltimer, 1024 launches
+    unsigned long long* gtrace = nullptr;       // SV_GTRACE: GEMM phase stamps [1024][8][2] of traced steps
     bool trace_env = false;                     // SV_KTRACE: trace every step, CSV at sv_wait_final
     bool trace_next = false;                    // sv_debug_trace_next: trace the next submit
     bool trace_valid = false;                   // the last submit was traced
@@ -462,8 +465,9 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (getenv("SV_SPLIT_ANY")) g_split_any = true;
     if (getenv("SV_NO_BOX")) e->no_box = true;
     if (getenv("SV_NO_WAVE")) e->no_wave = true;
+    if (getenv("SV_NO_WARM")) e->no_warm = true;
     if (getenv("SV_NO_T160")) e->no_t160 = true;
-    if (getenv("SV_ATTN_PF")) e->attn_pf = true;
+    if (const char* ap = getenv("SV_ATTN_PF")) e->attn_pf = atoi(ap);
     e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
     e->L = cfg->n_layers; e->d = cfg->d_model; e->F = cfg->d_ff; e->V = cfg->vocab;
     e->H = cfg->n_heads; e->D = cfg->head_dim;
@@ -490,6 +494,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
     CK(cudaMalloc((void**)&e->ktrace_buf, 1024 * 2 * sizeof(unsigned long long)));
     e->trace_env = getenv("SV_KTRACE") != nullptr;
+    if (getenv("SV_GTRACE")) CK(cudaMalloc((void**)&e->gtrace, 1024 * 32 * sizeof(unsigned long long)));
     if (getenv("SV_ATRACE")) CK(cudaMalloc((void**)&e->atrace, (size_t)e->L * 16 * sizeof(unsigned long long)));
     *out = e;
     return SV_OK;
@@ -546,7 +551,7 @@ extern "C" sv_status sv_engine_destroy(sv_engine* e) {
                    e->attn_o, e->attn_ml, e->u, e->u_exit, e->attn_out, e->act, e->cnt_main, e->cnt_exit,
                    e->cnt_attn, e->cnt_acc_exit, e->cnt_acc_final, e->stats_exit, e->stats_final, e->race_exit,
                    e->race_final, e->res_exit_dev, e->res_final_dev, e->meta_dev, e->probs_stage,
-                   e->h_exit, e->ssq_ad, e->act_ad, e->u_ad, e->stamps_dev, e->ktrace_buf, e->atrace};
+                   e->h_exit, e->ssq_ad, e->act_ad, e->u_ad, e->stamps_dev, e->ktrace_buf, e->atrace, e->gtrace};
     for (void* p : dev)
         if (p) cudaFree(p);
     cudaFreeHost(e->meta_host);
@@ -694,6 +699,9 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
     e->kmeta.clear();
     if (e->ktrace && (r = cudaMemsetAsync(e->ktrace, 0xFF, 1024 * 2 * sizeof(unsigned long long), st)) != cudaSuccess)
         return r;
+    if (e->ktrace && e->gtrace &&
+        (r = cudaMemsetAsync(e->gtrace, 0xFF, 1024 * 32 * sizeof(unsigned long long), st)) != cudaSuccess)
+        return r;
     EmbedArgs ea{(const int32_t*)(e->meta_dev + e->off_tok), e->embed, e->norm_attn[0], e->h, e->u, ssq_at(e, 0, 0), M,
                  e->MP, d};
     ea.ktrace = e->ktrace;
@@ -723,6 +731,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         a.counters = exit_ws ? e->cnt_exit : e->cnt_main;
         a.ktrace = e->ktrace;
         a.ktrace_id = nl;
+        a.gtrace = e->ktrace ? e->gtrace : nullptr;
+        a.warm = e->no_warm ? 0 : 1;
         // persistent path (M > 128): wave-aware token tile, 128 or 256 rows, minimising
         // ceil(tiles / SMs) x tile (C4 at 1 GPU: O / down 160 -> 320 tiles, 2 -> 3 rounds of half size)
         // 160-token tiles (UMMA N = 160) fill the rounds of M = 640 / 1280 (C4 at 1-2 GPUs)
@@ -791,6 +801,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         aa.ktrace = e->ktrace;
         aa.ktrace_id = nl;
         aa.ready_stamp = e->stamps_dev + stamp_slot;
+        aa.gtrace = e->ktrace ? e->gtrace : nullptr;
         {
             cudaEvent_t _a = pbeg(s);
             if ((q = accept_launch(aa, s)) != cudaSuccess) return q;
@@ -839,6 +850,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             if (e->attn_pf) {
                 aa.pf_ptr = e->w_o[l];
                 aa.pf_bytes = (size_t)d * d * 2;
+                aa.pf_early = e->attn_pf == 2;
             }
             LAUNCH(SV_K_ATTN, l, st, attn_bytes, attn_flops,
                    e->D == 128 ? attn3_launch(aa, e->attn_splits > 0 ? e->attn_splits : attn3_splits(nA, e->H, nchunk, e->num_sms), max_ctx, st)
@@ -1270,6 +1282,21 @@ extern "C" sv_status sv_wait_final(sv_ticket* t, int64_t timeout_us) {
                 for (size_t i = 0; i < e->last_kmeta.size(); ++i)
                     fprintf(fp, "%zu,%d,%d,%llu,%llu\n", i, e->last_kmeta[i].kind, e->last_kmeta[i].layer, tr[2 * i],
                             ~tr[2 * i + 1]);
+                fclose(fp);
+            }
+        }
+    }
+    if (e->gtrace && e->trace_valid) {   // GEMM phase stamps of this traced step (SV_GTRACE=<csv>)
+        std::vector<unsigned long long> tr((size_t)1024 * 32);
+        if (cudaMemcpy(tr.data(), e->gtrace, tr.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            FILE* fp = fopen(getenv("SV_GTRACE"), "w");
+            if (fp) {
+                fprintf(fp, "id,kind,layer,phase,first_ns,last_ns\n");
+                for (size_t i = 0; i < e->last_kmeta.size(); ++i)
+                    for (int p = 0; p < 16; ++p)
+                        if (tr[(i * 16 + p) * 2] != ~0ull)
+                            fprintf(fp, "%zu,%d,%d,%d,%llu,%llu\n", i, e->last_kmeta[i].kind, e->last_kmeta[i].layer, p,
+                                    tr[(i * 16 + p) * 2], ~tr[(i * 16 + p) * 2 + 1]);
                 fclose(fp);
             }
         }

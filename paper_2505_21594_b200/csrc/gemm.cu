@@ -57,7 +57,7 @@ struct GemmCfg {
     static constexpr int STAGE = A_STAGE + B_STAGE;
     // small token tiles: SV_GEMM_CTAS_PER_SM CTAs per SM (two grids co-resident
     // under programmatic dependent launch), else 1 CTA per SM
-    static constexpr int AUX = 2048;        // barriers, tmem slot, rstd[TN], reductions
+    static constexpr int AUX = 2304;        // barriers, tmem slot, rstd[TN], reductions, token metadata
     static constexpr int BUDGET =
         (TN <= 64 ? (228 * 1024) / SV_GEMM_CTAS_PER_SM - 1024 : 225 * 1024) - 1024 - AUX;
     static constexpr int STAGES_RAW = BUDGET / STAGE;
@@ -69,16 +69,12 @@ struct GemmCfg {
     static_assert((TN + EPI_CHUNK) * TM * 4 <= STAGES * STAGE, "split partial + epilogue tile");
 };
 
-struct GemmCtaSync {
-    __device__ void operator()() const { __syncthreads(); }
+// barrier of the tail: all 128 threads (barrier 0) in the real pass, warps 2-3
+// (barrier 1, 64 threads) in the warm-up pass
+struct EpiBar {
+    int id, cnt;
+    __device__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
 };
-
-template <int EPI>
-__device__ __forceinline__ void epi_chunk(const GemmArgs& a, const float* sOut, const float* sR, float* sRed,
-                                          int tok0, int m0, int n0, int nt, const int* sPos, const int* sBlk,
-                                          const float* hpre = nullptr) {
-    epi_apply<EPI>(a, sOut, sR, sRed, tok0, m0, n0, nt, (int)threadIdx.x, GemmCtaSync{}, sPos, sBlk, hpre);
-}
 
 template <int TN, int EPI>
 __global__ void __launch_bounds__(128, 1)
@@ -97,6 +93,7 @@ __global__ void __launch_bounds__(128, 1)
     int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
     float* sR = reinterpret_cast<float*>(aux + 256);          // [TN]
     float* sRed = sR + 256;                                   // [4][EPI_CHUNK]
+    float* sRedDry = reinterpret_cast<float*>(aux + 2048);    // [4][EPI_CHUNK] (warm-up pass)
     int* sPos = reinterpret_cast<int*>(aux + 1536);           // [TN <= 64] (EPI_QKV token metadata)
     int* sBlk = sPos + 64;
     float* sOut = reinterpret_cast<float*>(smem);             // [EPI_CHUNK][128], reuses the ring
@@ -104,6 +101,8 @@ __global__ void __launch_bounds__(128, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nt = blockIdx.x, mt = blockIdx.y, split = blockIdx.z;
     ktrace_mark(a.ktrace, a.ktrace_id, 0);
+    unsigned long long* gtr = threadIdx.x == 0 ? a.gtrace : nullptr;
+    gphase_mark(gtr, a.ktrace_id, 0);
     const int NT = gridDim.x, MT = gridDim.y;
     const int n0 = nt * TM, m0 = mt * TN;
     const int KB = a.K / BK;
@@ -143,6 +142,7 @@ __global__ void __launch_bounds__(128, 1)
             tma_load_2d(&tmA, sA + i * A_STAGE, &full[i], (kb0 + i) * BK, n0, pol_w);
         }
         pdl_wait();
+        gphase_mark(gtr, a.ktrace_id, 1);
         for (int i = 0; i < pre; ++i) tma_load_2d(&tmB, sB + i * C::B_STAGE, &full[i], (kb0 + i) * BK, m0 + a.b_row0, pol_x);
         for (int i = pre; i < nk; ++i) {
             const int s = i % C::STAGES;
@@ -178,71 +178,101 @@ __global__ void __launch_bounds__(128, 1)
         umma_commit(done);
     }
     __syncwarp();
-    pdl_wait();   // everything below reads data produced by the previous kernel
 
-    // warps 2-3 (idle during the mainloop) stage what the epilogue needs while the
-    // tensor core still runs: rstd of the folded RMSNorm (fixed summation order) and,
-    // for the QKV epilogue, each token's position and KV page
+    // The tail below (TMEM -> partials / epilogue, split-K ticket and reduction)
+    // runs once per CTA, so its instructions are cold in the SM's instruction cache
+    // and it sits on the step's critical path.  Warps 2-3, idle until the
+    // accumulator is ready, first run the very same code as a dry pass (pass 0:
+    // every store and atomic predicated off, their own 64-thread barrier, before
+    // griddepcontrol.wait), so the real pass (pass 1, all 128 threads) runs warm.
     constexpr bool kStageMeta = (EPI == EPI_QKV && TN <= 64);
-    if (warp >= 2) {
-        epi_rstd(a, sR, m0, TN, threadIdx.x - 64, 64);
-        if constexpr (kStageMeta) epi_meta(a, sPos, sBlk, m0, TN, threadIdx.x - 64, 64);
-    }
-    // residual epilogue of a single 16-token tile: this thread's residual column
-    // is loaded before the accumulator is ready (one round trip off the tail)
-    constexpr bool kPreH = (EPI == EPI_RESID && TN == 16);
-    float hpre[16];
-    if constexpr (kPreH) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-            hpre[j] = (m0 + j < a.M) ? __ldcg(&a.h[(size_t)(m0 + j) * a.d_model + n0 + threadIdx.x]) : 0.f;
-    }
-
-    mbar_wait(done, 0);
-    tc_fence_after();
-
+    constexpr bool kPre = (EPI == EPI_RESID || EPI == EPI_QKV) && TN == 16;
+    EpiPre pre;
     const int row = warp * 32 + lane;
     const uint32_t tbase = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     const bool direct = (a.splits == 1);
-    for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
-        if (m0 + c0 >= a.M) break;                       // CTA-uniform
-        uint32_t r[16];
-        tmem_ld_32x32b_x16(tbase + c0, r);
-        tmem_ld_wait();
-        if (direct) {
-            __syncthreads();                             // sR visible / previous chunk consumed
+    if (warp >= 2 && a.warm && kStageMeta)   // valid (zero) token metadata for the warm-up pass's loads
+        for (int t = threadIdx.x - 64; t < TN; t += 64) sPos[t] = sBlk[t] = 0;
+    for (int pass = (warp >= 2 && a.warm) ? 0 : 1; pass < 2; ++pass) {
+        const bool dry = pass == 0;
+        const EpiBar bar{dry ? 1 : 0, dry ? 64 : 128};
+        float* sRedP = dry ? sRedDry : sRed;
+        if (dry && kStageMeta) bar();
+        if (!dry) {
+            pdl_wait();   // everything below reads data produced by the previous kernel
+            gphase_mark(gtr, a.ktrace_id, 1);
+            // warps 2-3 (idle during the mainloop) stage what the epilogue needs while the
+            // tensor core still runs: rstd of the folded RMSNorm (fixed summation order) and,
+            // for the QKV epilogue, each token's position and KV page
+            if (warp >= 2) {
+                epi_rstd(a, sR, m0, TN, threadIdx.x - 64, 64);
+                if constexpr (kStageMeta) epi_meta(a, sPos, sBlk, m0, TN, threadIdx.x - 64, 64);
+            }
+            // single 16-token tile: every input of the epilogue that does not depend on the
+            // accumulator is loaded before it is ready (EpiPre), so the tail — the split-K
+            // reducer's in particular — has no load round trip of its own
+            if constexpr (kPre && EPI == EPI_RESID) {
+                const int r = threadIdx.x;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) sOut[j * TM + row] = __uint_as_float(r[j]);
-            __syncthreads();
-            epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt, kStageMeta ? sPos : nullptr,
-                               kStageMeta ? sBlk : nullptr, kPreH ? hpre : nullptr);
-        } else {
-            float* wsp = a.ws + (((size_t)split * NT + nt) * a.MP) * TM;
+                for (int j = 0; j < 16; ++j)
+                    pre.h[j] = (m0 + j < a.M) ? __ldcg(&a.h[(size_t)(m0 + j) * a.d_model + n0 + r]) : 0.f;
+                pre.g = __bfloat162float(reinterpret_cast<const bf16*>(a.g_out)[n0 + r]);
+                pre.g2 = a.u_out2 ? __bfloat162float(reinterpret_cast<const bf16*>(a.g_out2)[n0 + r]) : 0.f;
+            }
+            if constexpr (kPre && EPI == EPI_QKV) {
+                const int D = a.head_dim, half = D >> 1, i = ((n0 % a.d_model) + (int)threadIdx.x) % D;
+                const bool rot = n0 / a.d_model < 2;    // q and k sections
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int tok = m0 + c0 + j;
-                if (tok < a.M) __stcg(&wsp[(size_t)tok * TM + row], __uint_as_float(r[j]));
+                for (int j = 0; j < 16; ++j)
+                    pre.cs[j] = (rot && m0 + j < a.M)
+                                    ? reinterpret_cast<const float2*>(a.rope_cs)[(size_t)a.meta.pos[m0 + j] * half + i % half]
+                                    : make_float2(1.f, 0.f);
+            }
+            mbar_wait(done, 0);
+            tc_fence_after();
+            gphase_mark(gtr, a.ktrace_id, 2);
+        }
+
+        for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
+            if (m0 + c0 >= a.M) break;                       // CTA-uniform
+            uint32_t r[16];
+            if (!dry) {
+                tmem_ld_32x32b_x16(tbase + c0, r);
+                tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) r[j] = 0u;
+            }
+            if (direct) {
+                bar();                                       // sR visible / previous chunk consumed
+                if (!dry)
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) sOut[j * TM + row] = __uint_as_float(r[j]);
+                bar();
+                epi_apply<EPI>(a, sOut, sR, sRedP, m0 + c0, m0, n0, nt, row, bar, kStageMeta ? sPos : nullptr,
+                               kStageMeta ? sBlk : nullptr, kPre ? &pre : nullptr, dry);
+            } else if (!dry) {
+                float* wsp = a.ws + (((size_t)split * NT + nt) * a.MP) * TM;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int tok = m0 + c0 + j;
+                    if (tok < a.M) __stcg(&wsp[(size_t)tok * TM + row], __uint_as_float(r[j]));
+                }
             }
         }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
-    if (direct) {
-        ktrace_mark(a.ktrace, a.ktrace_id, 1);
-        return;
-    }
+        if (direct) continue;
 
-    {
         // ---------------- split-K through global memory: the last CTA of the tile
         // (atomic ticket) adds the partials in split order (deterministic; measured
         // faster at batch 1 than a cluster DSMEM reduction: C2 3.22 vs 3.34 ms)
         // CTA barrier + one acq_rel ticket by thread 0 (release covers the CTA's
         // partial stores through the barrier; acquire for the reducer's loads)
-        __syncthreads();
-        if (threadIdx.x == 0) *s_flag = (atomic_add_acq_rel(&a.counters[nt * MT + mt], 1) == a.splits - 1);
-        __syncthreads();
-        if (*s_flag) {
+        bar();
+        if (!dry && threadIdx.x == 0) *s_flag = (atomic_add_acq_rel(&a.counters[nt * MT + mt], 1) == a.splits - 1);
+        if (!dry) gphase_mark(gtr, a.ktrace_id, 3);
+        bar();
+        if (dry || *s_flag) {
+            if (!dry) gphase_mark(gtr, a.ktrace_id, 4);
             const size_t sstride = (size_t)NT * a.MP * TM;
             for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
                 if (m0 + c0 >= a.M) break;
@@ -281,18 +311,26 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
                     for (int j = 0; j < EPI_CHUNK; ++j) acc[j] += (j < nv) ? __ldcg(base + q * sstride + j * TM) : 0.f;
                 }
-                __syncthreads();
+                if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 7);
+                bar();
+                if (!dry)
 #pragma unroll
-                for (int j = 0; j < EPI_CHUNK; ++j) sOut[j * TM + row] = acc[j];
-                __syncthreads();
-                epi_chunk<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt, kStageMeta ? sPos : nullptr,
-                               kStageMeta ? sBlk : nullptr, kPreH ? hpre : nullptr);
+                    for (int j = 0; j < EPI_CHUNK; ++j) sOut[j * TM + row] = acc[j];
+                bar();
+                if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 8);
+                epi_apply<EPI>(a, sOut, sR, sRedP, m0 + c0, m0, n0, nt, row, bar, kStageMeta ? sPos : nullptr,
+                               kStageMeta ? sBlk : nullptr, kPre ? &pre : nullptr, dry);
+                if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 9);
             }
-            if (threadIdx.x == 0) a.counters[nt * MT + mt] = 0;
+            if (!dry && threadIdx.x == 0) a.counters[nt * MT + mt] = 0;
+            if (!dry) gphase_mark(gtr, a.ktrace_id, 6);
         }
-        ktrace_mark(a.ktrace, a.ktrace_id, 1);
-        return;
     }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) tmem_dealloc(tmem, C::TMEM_COLS);
+    gphase_mark(gtr, a.ktrace_id, 5);
+    ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 
 // ------------------------------------------------------------------ host side

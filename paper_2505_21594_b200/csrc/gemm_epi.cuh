@@ -20,13 +20,25 @@ constexpr int EPI_TM = 128;       // weight rows per tile
 constexpr int EPI_CHUNK = 16;     // token columns per epilogue pass
 constexpr int EPI_PAGE = 64;      // KV page size (sv_model_cfg.page_tokens is required to be 64)
 
+// Inputs of a single 16-token tile's epilogue that do not depend on the
+// accumulator, loaded by every thread while the tensor core still runs (so the
+// split-K reducer's tail has no load round trip of its own): the residual column
+// and the norm gains (EPI_RESID), RoPE cos/sin of the thread's dimension (EPI_QKV).
+struct EpiPre {
+    float h[EPI_CHUNK];
+    float g, g2;
+    float2 cs[EPI_CHUNK];
+};
+
 // sPos / sBlk (optional, EPI_QKV): position and KV page of token m0 + t, staged in
 // shared memory once per tile (epi_meta) instead of re-gathered per chunk.
 template <int EPI, class Sync>
 __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, const float* sR, float* sRed,
                                           int tok0, int m0, int n0, int nt, int r, Sync sync,
                                           const int* sPos = nullptr, const int* sBlk = nullptr,
-                                          const float* hpre = nullptr) {
+                                          const EpiPre* pre = nullptr, bool dry = false) {
+    // dry: the instruction-cache warm-up pass of gemm_kernel — the same code with
+    // every global store predicated off
     constexpr int TM = EPI_TM;
     const int warp = r >> 5, lane = r & 31;
     if constexpr (EPI == EPI_QKV) {
@@ -69,8 +81,9 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
         if (sec < 2) {
 #pragma unroll
             for (int j = 0; j < EPI_CHUNK; ++j)
-                cs[j] = (j < nv) ? reinterpret_cast<const float2*>(a.rope_cs)[(size_t)pos[j] * half + ih]
-                                 : make_float2(1.f, 0.f);
+                cs[j] = pre ? pre->cs[j]
+                            : ((j < nv) ? reinterpret_cast<const float2*>(a.rope_cs)[(size_t)pos[j] * half + ih]
+                                        : make_float2(1.f, 0.f));
         }
 #pragma unroll
         for (int j = 0; j < EPI_CHUNK; ++j) {
@@ -82,7 +95,8 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
                 const float vp = sOut[j * TM + rp] * rs;
                 v = (i < half) ? (v * cs[j].x - vp * cs[j].y) : (v * cs[j].x + vp * cs[j].y);
             }
-            if (sec == 0) {
+            if (dry) {
+            } else if (sec == 0) {
                 a.qbuf[(size_t)tok * d + col] = v;
             } else {
                 const int slot = pos[j] & (EPI_PAGE - 1);
@@ -92,28 +106,31 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
         }
     } else if constexpr (EPI == EPI_RESID) {
         const int d = a.d_model;
-        const float g = __bfloat162float(reinterpret_cast<const bf16*>(a.g_out)[n0 + r]);
-        const float g2 = a.u_out2 ? __bfloat162float(reinterpret_cast<const bf16*>(a.g_out2)[n0 + r]) : 0.f;
+        const float g = pre ? pre->g : __bfloat162float(reinterpret_cast<const bf16*>(a.g_out)[n0 + r]);
+        const float g2 = pre ? pre->g2
+                             : (a.u_out2 ? __bfloat162float(reinterpret_cast<const bf16*>(a.g_out2)[n0 + r]) : 0.f);
         const int nv = min(EPI_CHUNK, a.M - tok0);
         float hv[EPI_CHUNK];
 #pragma unroll
         for (int j = 0; j < EPI_CHUNK; ++j)          // all residual loads in flight first
-            hv[j] = hpre ? hpre[j] : ((j < nv) ? __ldcg(&a.h[(size_t)(tok0 + j) * d + n0 + r]) : 0.f);
+            hv[j] = pre ? pre->h[j] : ((j < nv) ? __ldcg(&a.h[(size_t)(tok0 + j) * d + n0 + r]) : 0.f);
 #pragma unroll
         for (int j = 0; j < EPI_CHUNK; ++j) {
-            if (j < nv) {
+            if (j < nv) hv[j] += sOut[j * TM + r];
+            if (j < nv && !dry) {
                 const size_t idx = (size_t)(tok0 + j) * d + n0 + r;
-                hv[j] += sOut[j * TM + r];
                 a.h[idx] = hv[j];
                 reinterpret_cast<bf16*>(a.u_out)[idx] = __float2bfloat16_rn(hv[j] * g);
                 if (a.h_out2) a.h_out2[idx] = hv[j];
                 if (a.u_out2) reinterpret_cast<bf16*>(a.u_out2)[idx] = __float2bfloat16_rn(hv[j] * g2);
             }
-            const float sq = warp_sum(hv[j] * hv[j]);
-            if (lane == 0) sRed[warp * EPI_CHUNK + j] = sq;
+            if (j < nv) {                            // (uniform) only the live tokens' sums
+                const float sq = warp_sum(hv[j] * hv[j]);
+                if (lane == 0) sRed[warp * EPI_CHUNK + j] = sq;
+            }
         }
         sync();
-        if (r < EPI_CHUNK && tok0 + r < a.M) {
+        if (r < EPI_CHUNK && tok0 + r < a.M && !dry) {
             const float s = (sRed[0 * EPI_CHUNK + r] + sRed[1 * EPI_CHUNK + r]) +
                             (sRed[2 * EPI_CHUNK + r] + sRed[3 * EPI_CHUNK + r]);
             a.ssq_out[(size_t)nt * a.MP + tok0 + r] = s;
@@ -127,20 +144,20 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
             const float g = sOut[j * TM + rr] * rs;
             const float u = sOut[j * TM + 64 + rr] * rs;
             const float y = g / (1.0f + expf(-g)) * u;
-            reinterpret_cast<bf16*>(a.act)[(size_t)tok * a.d_ff + nt * 64 + rr] = __float2bfloat16_rn(y);
+            if (!dry) reinterpret_cast<bf16*>(a.act)[(size_t)tok * a.d_ff + nt * 64 + rr] = __float2bfloat16_rn(y);
         }
     } else if constexpr (EPI == EPI_SILU) {
         for (int j = 0; j < EPI_CHUNK; ++j) {
             const int tok = tok0 + j;
             if (tok >= a.M) break;
             const float x = sOut[j * TM + r] * sR[tok - m0];
-            reinterpret_cast<bf16*>(a.act)[(size_t)tok * a.N + n0 + r] = __float2bfloat16_rn(x / (1.0f + expf(-x)));
+            if (!dry) reinterpret_cast<bf16*>(a.act)[(size_t)tok * a.N + n0 + r] = __float2bfloat16_rn(x / (1.0f + expf(-x)));
         }
     } else {  // EPI_LOGITS
         for (int j = 0; j < EPI_CHUNK; ++j) {
             const int tok = tok0 + j;
             if (tok >= a.M) break;
-            a.logits[(size_t)tok * a.N + n0 + r] = sOut[j * TM + r] * sR[tok - m0];
+            if (!dry) a.logits[(size_t)tok * a.N + n0 + r] = sOut[j * TM + r] * sR[tok - m0];
         }
     }
 }

@@ -64,6 +64,8 @@ struct GemmArgs {
     // this grid's tail, the launch gap and the next grid's ramp-up.
     const CUtensorMap* pf_map = nullptr;    // device copy of the next weight map, or nullptr
     int pf_tiles = 0, pf_splits = 1, pf_kb = 0, pf_depth = 0;
+    unsigned long long* gtrace = nullptr;   // optional phase stamps [launch][16][2] (SV_GTRACE)
+    int warm = 0;         // gemm_kernel: warps 2-3 run the tail once as a dry pass (instruction-cache warm-up)
     unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
     int ktrace_id = 0;
 };
@@ -102,6 +104,7 @@ struct AttnArgs {
     // QKV GEMM has completed: attention is latency-bound and leaves HBM idle
     const void* pf_ptr = nullptr;
     size_t pf_bytes = 0;
+    int pf_early = 0;     // issue that prefetch at kernel start (before griddepcontrol.wait)
     int num_sms = 0;      // SMs of the engine's device (occupancy choice of attn3)
 };
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st);
@@ -143,6 +146,7 @@ struct AcceptArgs {
     unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
     int ktrace_id = 0;
     unsigned long long* ready_stamp = nullptr;   // globaltimer when the last request's result was written (max)
+    unsigned long long* gtrace = nullptr;        // optional phase stamps (SV_GTRACE): row_stats at ktrace_id + 1
 };
 cudaError_t accept_launch(const AcceptArgs& a, cudaStream_t st);
 int accept_chunks(int V, int* chunk);
