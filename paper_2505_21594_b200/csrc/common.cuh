@@ -191,6 +191,17 @@ __device__ __forceinline__ void gphase_mark(unsigned long long* tr, int id, int 
     }
 }
 
+// 64-bit relaxed accesses at gpu scope: single-copy atomic, so a (value, tag) pair
+// written by one CTA is seen by another either whole or not at all (no fence)
+__device__ __forceinline__ void st_relaxed_b64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_b64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // ticket for "the last CTA to arrive does the merge": one acq_rel atomic by the
 // calling thread (release: its prior writes and, after a CTA barrier, the CTA's;
 // acquire: the other arrivals' writes for the merge that follows)

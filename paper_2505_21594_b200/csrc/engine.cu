@@ -224,6 +224,7 @@ struct sv_engine {
     bool no_t160 = false;                       // env SV_NO_T160: no 160-token persistent tiles
     bool no_wave = false;                       // env SV_NO_WAVE: always 256-token tiles above 128 rows
     bool no_warm = false;                       // env SV_NO_WARM: no instruction-cache warm-up pass in gemm_kernel
+    int o_mode = 0;                             // env SV_O_MODE: bit 0 small ring, bit 1 L2 staging of O's weights
     int attn_pf = 0;                            // attention prefetches the O weights to L2 (env SV_ATTN_PF=1 after
                                                 // griddepcontrol.wait, 2 before it)
     int attn_splits = 0;                        // attention split override (env SV_ATTN_SPLITS; 0 = attn3_splits)
@@ -263,7 +264,9 @@ struct sv_engine {
     float* probs_stage = nullptr;               // device copy of host draft probs
     // per-step metadata (device + pinned staging, same layout)
     uint8_t *meta_dev, *meta_host;
-    size_t meta_bytes, off_tok, off_pos, off_req, off_ctx, off_pt, off_reqdev, off_seq, off_grows, off_cpre;
+    size_t meta_bytes, off_tok, off_pos, off_req, off_ctx, off_pt, off_reqdev, off_seq, off_grows, off_cpre, off_epoch;
+    uint32_t epoch = 0;                         // meta epoch: split-K partial tags (GemmArgs::sk_tagged)
+    bool sk_ticket = false;                     // env SV_SK_TICKET: atomic-ticket split-K reduction
     // pinned mailboxes
     sv_exit_result *mb_exit, *mb_final;
     volatile uint64_t* mb_flag;
@@ -330,8 +333,8 @@ static sv_status engine_alloc(sv_engine* e) {
         }
     }
     e->ws_elems = ws;
-    CK(dalloc((void**)&e->ws_main, ws * 4));
-    CK(dalloc((void**)&e->ws_exit, ws * 4));
+    CK(dalloc((void**)&e->ws_main, ws * 8));   // (value, tag) pairs
+    CK(dalloc((void**)&e->ws_exit, ws * 8));
     const int max_tiles = std::max({3 * d, 2 * F, V}) / 128 * (MP / 16 + 1);
     CK(dalloc((void**)&e->cnt_main, (size_t)max_tiles * 4));
     CK(dalloc((void**)&e->cnt_exit, (size_t)max_tiles * 4));
@@ -381,6 +384,7 @@ static sv_status engine_alloc(sv_engine* e) {
     e->off_cpre = off; off = align_up(off + (size_t)VB * 4, 256);
     e->off_reqdev = off; off = align_up(off + (size_t)B * sizeof(ReqDev), 256);
     e->off_seq = off; off = align_up(off + 8, 256);
+    e->off_epoch = off; off = align_up(off + 8, 256);
     e->meta_bytes = off;
     CK(dalloc((void**)&e->meta_dev, off));
     CK(cudaMallocHost((void**)&e->meta_host, off));
@@ -466,6 +470,8 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (getenv("SV_NO_BOX")) e->no_box = true;
     if (getenv("SV_NO_WAVE")) e->no_wave = true;
     if (getenv("SV_NO_WARM")) e->no_warm = true;
+    if (getenv("SV_SK_TICKET")) e->sk_ticket = true;
+    if (const char* om = getenv("SV_O_MODE")) e->o_mode = atoi(om);
     if (getenv("SV_NO_T160")) e->no_t160 = true;
     if (const char* ap = getenv("SV_ATTN_PF")) e->attn_pf = atoi(ap);
     e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
@@ -646,6 +652,8 @@ static GemmArgs base_args(sv_engine* e, int M) {
     a.meta.ctx = (int32_t*)(e->meta_dev + e->off_ctx);
     a.meta.page_table = (int32_t*)(e->meta_dev + e->off_pt);
     a.meta.pt_stride = e->pt_stride;
+    a.meta.epoch = (const uint32_t*)(e->meta_dev + e->off_epoch);
+    a.sk_tagged = (e->sk_ticket || g_split_any) ? 0 : 1;   // the tagged path reduces <= 8 splits
     return a;
 }
 
@@ -858,6 +866,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         }
         {   // O projection + residual
             GemmArgs a = base_args(e, M);
+            a.small_ring = (e->o_mode & 1) && tn == 16;
+            a.l2_rest = (e->o_mode & 2) && tn <= 64;
             a.h = e->h; a.g_out = e->norm_mlp[l]; a.u_out = e->u; a.ssq_out = ssq_at(e, l, 1);
             LAUNCH(SV_K_O, l, st, gemm_bytes(d, d, Md * 10 + (d / 128) * M * 4.0), 2.0 * M * d * d,
                    gemm(EPI_RESID, L + l, 1, d, d, a, st, false, 2 * L + l, 2 * F, d));
@@ -930,6 +940,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
 }
 
 static sv_status run_step(sv_engine* e, cudaStream_t st, int n, int gamma, uint64_t exit_mask, int nchunk) {
+    *(uint32_t*)(e->meta_host + e->off_epoch) = ++e->epoch & 0x3FFFFF;   // fresh split-K tags for this step
     CK(cudaMemcpyAsync(e->meta_dev, e->meta_host, e->meta_bytes, cudaMemcpyHostToDevice, st));
     int nl = 0;
     const bool trace = (e->trace_env || e->trace_next) && !e->prof;
@@ -1376,6 +1387,7 @@ static sv_status prefill_pass(sv_session* s, const int32_t* tokens, int32_t n, i
     rd->ctx = len;
     rd->probs = sample ? (uint64_t)e->logits_final : 0;   // gamma = 0: never read, non-zero = sample
     cudaStream_t st = e->s_cap;
+    *(uint32_t*)(mh + e->off_epoch) = ++e->epoch & 0x3FFFFF;   // fresh split-K tags for this pass
     CK(cudaMemcpyAsync(e->meta_dev, e->meta_host, e->meta_bytes, cudaMemcpyHostToDevice, st));
     e->pf.on = true;
     e->pf.all_rows = logits_dev != nullptr;

@@ -51,7 +51,7 @@ constexpr int A_STAGE = TM * BK * 2;        // 16 KB
 #define SV_GEMM_CTAS_PER_SM 2
 #endif
 
-template <int TN>
+template <int TN, int MAXST = SV_GEMM_MAX_STAGES>
 struct GemmCfg {
     static constexpr int B_STAGE = TN * BK * 2;
     static constexpr int STAGE = A_STAGE + B_STAGE;
@@ -61,7 +61,7 @@ struct GemmCfg {
     static constexpr int BUDGET =
         (TN <= 64 ? (228 * 1024) / SV_GEMM_CTAS_PER_SM - 1024 : 225 * 1024) - 1024 - AUX;
     static constexpr int STAGES_RAW = BUDGET / STAGE;
-    static constexpr int STAGES = STAGES_RAW > SV_GEMM_MAX_STAGES ? SV_GEMM_MAX_STAGES : STAGES_RAW;
+    static constexpr int STAGES = STAGES_RAW > MAXST ? MAXST : STAGES_RAW;
     static constexpr int TMEM_COLS = TN < 32 ? 32 : TN;
     static constexpr int SMEM = 1024 + STAGES * STAGE + AUX;
     static_assert(STAGES >= 2, "pipeline too shallow");
@@ -76,11 +76,11 @@ struct EpiBar {
     __device__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
 };
 
-template <int TN, int EPI>
+template <int TN, int EPI, int MAXST = SV_GEMM_MAX_STAGES>
 __global__ void __launch_bounds__(128, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ GemmArgs a) {
-    using C = GemmCfg<TN>;
+    using C = GemmCfg<TN, MAXST>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -141,6 +141,8 @@ __global__ void __launch_bounds__(128, 1)
             mbar_arrive_expect_tx(&full[i], stage_tx);
             tma_load_2d(&tmA, sA + i * A_STAGE, &full[i], (kb0 + i) * BK, n0, pol_w);
         }
+        if (a.l2_rest)   // the rest of this CTA's weight slice -> L2 (GemmArgs::l2_rest)
+            for (int i = pre; i < nk; ++i) tma_prefetch_l2_2d(&tmA, (kb0 + i) * BK, n0);
         pdl_wait();
         gphase_mark(gtr, a.ktrace_id, 1);
         for (int i = 0; i < pre; ++i) tma_load_2d(&tmB, sB + i * C::B_STAGE, &full[i], (kb0 + i) * BK, m0 + a.b_row0, pol_x);
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(128, 1)
     const int row = warp * 32 + lane;
     const uint32_t tbase = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     const bool direct = (a.splits == 1);
+    const uint32_t tag = (a.meta.epoch ? (*a.meta.epoch << 10) : 0u) | (uint32_t)(a.ktrace_id & 1023);
     if (warp >= 2 && a.warm && kStageMeta)   // valid (zero) token metadata for the warm-up pass's loads
         for (int t = threadIdx.x - 64; t < TN; t += 64) sPos[t] = sBlk[t] = 0;
     for (int pass = (warp >= 2 && a.warm) ? 0 : 1; pass < 2; ++pass) {
@@ -251,6 +254,15 @@ __global__ void __launch_bounds__(128, 1)
                 bar();
                 epi_apply<EPI>(a, sOut, sR, sRedP, m0 + c0, m0, n0, nt, row, bar, kStageMeta ? sPos : nullptr,
                                kStageMeta ? sBlk : nullptr, kPre ? &pre : nullptr, dry);
+            } else if (!dry && a.sk_tagged) {
+                if (split != 0) {   // split 0 keeps its partial in TMEM and reduces
+                    uint64_t* wsp = reinterpret_cast<uint64_t*>(a.ws) + (((size_t)split * NT + nt) * a.MP) * TM;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int tok = m0 + c0 + j;
+                        if (tok < a.M) st_relaxed_b64(&wsp[(size_t)tok * TM + row], ((uint64_t)tag << 32) | r[j]);
+                    }
+                }
             } else if (!dry) {
                 float* wsp = a.ws + (((size_t)split * NT + nt) * a.MP) * TM;
 #pragma unroll
@@ -261,6 +273,78 @@ __global__ void __launch_bounds__(128, 1)
             }
         }
         if (direct) continue;
+
+        if (a.sk_tagged) {
+            // ---------------- split-K, tagged partials: every split but 0 stores (value,
+            // tag) pairs with single 64-bit relaxed stores and is done; split 0 reloads its
+            // own partial from TMEM and polls the others' pairs until they carry this
+            // launch's tag (step epoch, launch index): no fence, no ticket, one round trip
+            // when the partials are already there.  Sum in split order 0..S-1 (the same
+            // arithmetic as the ticketed path: deterministic).
+            if (split != 0 && !dry) continue;
+            if (!dry) gphase_mark(gtr, a.ktrace_id, 4);
+            const size_t sstride = (size_t)NT * a.MP * TM;
+            for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
+                if (m0 + c0 >= a.M) break;
+                const int nv = min(EPI_CHUNK, a.M - (m0 + c0));
+                float acc[EPI_CHUNK];
+                {
+                    uint32_t r[16];
+                    if (!dry) {
+                        tmem_ld_32x32b_x16(tbase + c0, r);
+                        tmem_ld_wait();
+                    }
+#pragma unroll
+                    for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = dry ? 0.f : 0.f + __uint_as_float(r[j]);
+                }
+                const uint64_t* base = reinterpret_cast<const uint64_t*>(a.ws) + ((size_t)nt * a.MP + m0 + c0) * TM + row;
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {         // 8 tokens x 7 splits per round trip
+                    if (g * 8 >= nv) break;
+                    uint64_t x[7][8];
+#pragma unroll
+                    for (int u = 0; u < 7; ++u)
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            x[u][j] = (u + 1 < a.splits && g * 8 + j < nv)
+                                          ? ld_relaxed_b64(base + (u + 1) * sstride + (g * 8 + j) * TM)
+                                          : ((uint64_t)tag << 32);
+                    if (!dry) {
+                        uint32_t n = 0;
+                        for (;;) {   // re-load the pairs that do not carry this launch's tag yet
+                            bool ok = true;
+#pragma unroll
+                            for (int u = 0; u < 7; ++u)
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    if ((uint32_t)(x[u][j] >> 32) != tag) {
+                                        ok = false;
+                                        x[u][j] = ld_relaxed_b64(base + (u + 1) * sstride + (g * 8 + j) * TM);
+                                    }
+                            if (ok) break;
+                            if (++n > SV_SPIN_LIMIT) __trap();
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+#pragma unroll
+                        for (int u = 0; u < 7; ++u)
+                            if (u + 1 < a.splits && g * 8 + j < nv) acc[g * 8 + j] += __uint_as_float((uint32_t)x[u][j]);
+                }
+                if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 7);
+                bar();
+                if (!dry)
+#pragma unroll
+                    for (int j = 0; j < EPI_CHUNK; ++j) sOut[j * TM + row] = acc[j];
+                bar();
+                if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 8);
+                epi_apply<EPI>(a, sOut, sR, sRedP, m0 + c0, m0, n0, nt, row, bar, kStageMeta ? sPos : nullptr,
+                               kStageMeta ? sBlk : nullptr, kPre ? &pre : nullptr, dry);
+                if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 9);
+            }
+            if (!dry) gphase_mark(gtr, a.ktrace_id, 6);
+            continue;
+        }
 
         // ---------------- split-K through global memory: the last CTA of the tile
         // (atomic ticket) adds the partials in split order (deterministic; measured
@@ -381,24 +465,24 @@ int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms) {
     return s;
 }
 
-template <int TN, int EPI>
+template <int TN, int EPI, int MAXST = SV_GEMM_MAX_STAGES>
 static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, cudaStream_t st) {
-    using C = GemmCfg<TN>;
+    using C = GemmCfg<TN, MAXST>;
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_kernel<TN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(gemm_kernel<TN, EPI, MAXST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM);
         if (e != cudaSuccess) return e;
         if (!getenv("SV_NO_CARVEOUT")) {   // let two grids' CTAs share an SM (PDL co-residency)
-            e = cudaFuncSetAttribute(gemm_kernel<TN, EPI>, cudaFuncAttributePreferredSharedMemoryCarveout,
+            e = cudaFuncSetAttribute(gemm_kernel<TN, EPI, MAXST>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared);
             if (e != cudaSuccess) return e;
         }
         if (getenv("SV_GEMM_DEBUG")) {
             int nb = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gemm_kernel<TN, EPI>, 128, C::SMEM);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, gemm_kernel<TN, EPI, MAXST>, 128, C::SMEM);
             cudaFuncAttributes fa;
-            cudaFuncGetAttributes(&fa, gemm_kernel<TN, EPI>);
+            cudaFuncGetAttributes(&fa, gemm_kernel<TN, EPI, MAXST>);
             int dev = 0, smsm = 0, rsv = 0, optin = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
@@ -424,7 +508,7 @@ static cudaError_t launch_t(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<TN, EPI>, tmA, tmB, a);
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<TN, EPI, MAXST>, tmA, tmB, a);
 }
 
 template <int TN>
@@ -445,6 +529,9 @@ cudaError_t gemm_big_launch(int epi, int tile_n, const CUtensorMap& tmA, const C
 
 cudaError_t gemm_launch(int epi, int tile_n, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                         cudaStream_t st) {
+    // small-ring variant of the 16-token residual GEMM (GemmArgs::small_ring): 4 stages
+    // (76 KB), so the O projection's CTAs fit beside two attention CTAs
+    if (tile_n == 16 && epi == EPI_RESID && a.small_ring) return launch_t<16, EPI_RESID, 4>(tmA, tmB, a, st);
     // large token tiles without split-K: persistent kernel with overlapped epilogue
     if (tile_n >= 128 && a.splits == 1 && !getenv("SV_NO_BIG_GEMM")) return gemm_big_launch(epi, tile_n, tmA, tmB, a, st);
     switch (tile_n) {

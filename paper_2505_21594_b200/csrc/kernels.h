@@ -25,6 +25,7 @@ struct StepMeta {
     int32_t* row_req;     // [rows] request index of each query row
     int32_t* page_table;  // [B][pt_stride] KV block ids
     int32_t pt_stride;
+    const uint32_t* epoch;   // incremented by the host for every issued step (split-K partial tags)
 };
 
 struct GemmArgs {
@@ -33,7 +34,7 @@ struct GemmArgs {
     int splits;          // split-K factor (deterministic reduction, fixed order)
     int b_row0;          // first row of the activation tensor map (exit slot k: k * MP)
     int b_box;           // rows of the activation TMA box (<= tile_n; 0 = tile_n), M <= tile_n only
-    float* ws;           // split-K partials [splits][ntiles][MP][128]
+    float* ws;           // split-K partials [splits][ntiles][MP][128] (8 bytes per element)
     int* counters;       // [ntiles * mtiles], zero on entry, reset by the reducer
     // RMSNorm folding: rstd[m] = 1/sqrt(sum_t ssq_in[t][m] / d + eps)
     const float* ssq_in;  // [ssq_tiles][MP] or nullptr (no scaling)
@@ -66,6 +67,10 @@ struct GemmArgs {
     int pf_tiles = 0, pf_splits = 1, pf_kb = 0, pf_depth = 0;
     unsigned long long* gtrace = nullptr;   // optional phase stamps [launch][16][2] (SV_GTRACE)
     int warm = 0;         // gemm_kernel: warps 2-3 run the tail once as a dry pass (instruction-cache warm-up)
+    // the CTA's weight K blocks beyond its smem ring -> L2 before griddepcontrol.wait
+    int l2_rest = 0;
+    int small_ring = 0;   // 16-token EPI_RESID: 4-stage ring (co-resides with two attention CTAs)
+    int sk_tagged = 0;    // split-K: partials as (value, tag) pairs, split 0 reduces (else: atomic ticket)
     unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
     int ktrace_id = 0;
 };
