@@ -219,12 +219,10 @@ struct sv_engine {
     sv_model_cfg cfg;
     sv_engine_opts opts;
     int device, num_sms;
-    int pf_depth = 0;                           // GemmArgs::pf_depth (env SV_PF)
     bool no_box = false;                        // env SV_NO_BOX: load full token tiles
     bool no_t160 = false;                       // env SV_NO_T160: no 160-token persistent tiles
     bool no_wave = false;                       // env SV_NO_WAVE: always 256-token tiles above 128 rows
     bool no_warm = false;                       // env SV_NO_WARM: no instruction-cache warm-up pass in gemm_kernel
-    int o_mode = 0;                             // env SV_O_MODE: bit 0 small ring, bit 1 L2 staging of O's weights
     int attn_pf = 0;                            // attention prefetches the O weights to L2 (env SV_ATTN_PF=1 after
                                                 // griddepcontrol.wait, 2 before it)
     int attn_splits = 0;                        // attention split override (env SV_ATTN_SPLITS; 0 = attn3_splits)
@@ -265,15 +263,12 @@ struct sv_engine {
     // per-step metadata (device + pinned staging, same layout)
     uint8_t *meta_dev, *meta_host;
     size_t meta_bytes, off_tok, off_pos, off_req, off_ctx, off_pt, off_reqdev, off_seq, off_grows, off_cpre, off_epoch;
-    uint32_t epoch = 0;                         // meta epoch: split-K partial tags (GemmArgs::sk_tagged)
-    bool sk_ticket = false;                     // env SV_SK_TICKET: atomic-ticket split-K reduction
+    uint32_t epoch = 0;                         // meta epoch: split-K partial tags (gemm.cu)
     // pinned mailboxes
     sv_exit_result *mb_exit, *mb_final;
     volatile uint64_t* mb_flag;
     sv_exit_result* mb_exit_dev = nullptr;      // device aliases of the mapped mailboxes
     uint64_t* mb_flag_dev = nullptr;
-    // device-resident weight tensor maps (L2 prefetch of the next GEMM, env SV_PF)
-    CUtensorMap* d_tmaps = nullptr;             // [qkv L][o L][gu L][down L][lm]
     // tensor maps
     std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;
     CUtensorMap tm_lm;
@@ -431,7 +426,7 @@ static sv_status engine_tmaps(sv_engine* e) {
         if (!act_maps(e, tn, &m)) return fail(SV_E_DEVICE, "tensor map (activations)");
         e->tm_act[tn] = m;
     }
-    // device copy of the weight maps [qkv L][o L][gu L][down L][lm] (L2 prefetch, SV_PF)
+    // weight maps in launch-table order [qkv L][o L][gu L][down L][lm]
     const int L = e->L, nmaps = 4 * L + 1;
     std::vector<CUtensorMap> all(nmaps);
     for (int l = 0; l < L; ++l) {
@@ -441,8 +436,6 @@ static sv_status engine_tmaps(sv_engine* e) {
         all[3 * L + l] = e->tm_down[l];
     }
     all[4 * L] = e->tm_lm;
-    CK(cudaMalloc((void**)&e->d_tmaps, sizeof(CUtensorMap) * nmaps));
-    CK(cudaMemcpy(e->d_tmaps, all.data(), sizeof(CUtensorMap) * nmaps, cudaMemcpyHostToDevice));
     e->wmap128 = all;
     return SV_OK;
 }
@@ -462,16 +455,12 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     e->opts = *opts;
     e->device = device;
     CK(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device));
-    if (const char* pf = getenv("SV_PF")) e->pf_depth = atoi(pf);
     if (const char* as = getenv("SV_ATTN_SPLITS")) e->attn_splits = atoi(as);
     if (const char* ns = getenv("SV_ATTN_NST")) g_attn_nst = atoi(ns);
     if (const char* mb = getenv("SV_A3_MINB")) g_attn_minb = atoi(mb);
-    if (getenv("SV_SPLIT_ANY")) g_split_any = true;
     if (getenv("SV_NO_BOX")) e->no_box = true;
     if (getenv("SV_NO_WAVE")) e->no_wave = true;
     if (getenv("SV_NO_WARM")) e->no_warm = true;
-    if (getenv("SV_SK_TICKET")) e->sk_ticket = true;
-    if (const char* om = getenv("SV_O_MODE")) e->o_mode = atoi(om);
     if (getenv("SV_NO_T160")) e->no_t160 = true;
     if (const char* ap = getenv("SV_ATTN_PF")) e->attn_pf = atoi(ap);
     e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
@@ -552,7 +541,6 @@ extern "C" sv_status sv_engine_destroy(sv_engine* e) {
     cudaSetDevice(e->device);
     cudaDeviceSynchronize();
     for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
-    if (e->d_tmaps) cudaFree(e->d_tmaps);
     void* dev[] = {e->h, e->qbuf, e->ssq, e->logits_exit, e->logits_final, e->ws_main, e->ws_exit, e->rope,
                    e->attn_o, e->attn_ml, e->u, e->u_exit, e->attn_out, e->act, e->cnt_main, e->cnt_exit,
                    e->cnt_attn, e->cnt_acc_exit, e->cnt_acc_final, e->stats_exit, e->stats_final, e->race_exit,
@@ -653,7 +641,6 @@ static GemmArgs base_args(sv_engine* e, int M) {
     a.meta.page_table = (int32_t*)(e->meta_dev + e->off_pt);
     a.meta.pt_stride = e->pt_stride;
     a.meta.epoch = (const uint32_t*)(e->meta_dev + e->off_epoch);
-    a.sk_tagged = (e->sk_ticket || g_split_any) ? 0 : 1;   // the tagged path reduces <= 8 splits
     return a;
 }
 
@@ -728,11 +715,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         }
     }
 
-    // nx / nN / nK: the next GEMM on the same stream (its weights are prefetched to L2)
-    // wid: weight index in [qkv L][o L][gu L][down L][lm] order; nx: the next GEMM's
-    // weight index on the same stream (its first weights are prefetched to L2)
-    auto gemm = [&](int epi, int wid, int bbuf, int N, int K, GemmArgs a, cudaStream_t s, bool exit_ws, int nx = -1,
-                    int nN = 0, int nK = 0) -> cudaError_t {
+    // wid: weight index in [qkv L][o L][gu L][down L][lm] order
+    auto gemm = [&](int epi, int wid, int bbuf, int N, int K, GemmArgs a, cudaStream_t s, bool exit_ws) -> cudaError_t {
         a.N = N;
         a.K = K;
         a.ws = exit_ws ? e->ws_exit : e->ws_main;
@@ -774,13 +758,6 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             a.b_box = box;
         }
         const CUtensorMap& B = *Bp;
-        if (nx >= 0 && tn <= 64 && e->pf_depth > 0) {
-            a.pf_map = e->d_tmaps + nx;
-            a.pf_tiles = nN / 128;
-            a.pf_splits = gemm_pick_splits(nN, nK, M, tn, e->num_sms);
-            a.pf_kb = nK / 64;
-            a.pf_depth = e->pf_depth;
-        }
         return gemm_launch(epi, tl, A, B, a, s);
     };
     // slot >= 0: the exit reads u_exit slot `slot`; slot < 0: the adapter output u_ad
@@ -835,7 +812,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             a.ssq_in = ssq_at(e, l, 0);
             a.qbuf = e->qbuf;
             LAUNCH(SV_K_QKV, l, st, gemm_bytes(3.0 * d, d, Md * 8 + (d / 128) * M * 4.0), 2.0 * M * 3.0 * d * d,
-                   gemm(EPI_QKV, l, 0, 3 * d, d, a, st, false, L + l, d, d));
+                   gemm(EPI_QKV, l, 0, 3 * d, d, a, st, false));
         }
         {   // attention
             AttnArgs aa = {};
@@ -866,18 +843,16 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         }
         {   // O projection + residual
             GemmArgs a = base_args(e, M);
-            a.small_ring = (e->o_mode & 1) && tn == 16;
-            a.l2_rest = (e->o_mode & 2) && tn <= 64;
             a.h = e->h; a.g_out = e->norm_mlp[l]; a.u_out = e->u; a.ssq_out = ssq_at(e, l, 1);
             LAUNCH(SV_K_O, l, st, gemm_bytes(d, d, Md * 10 + (d / 128) * M * 4.0), 2.0 * M * d * d,
-                   gemm(EPI_RESID, L + l, 1, d, d, a, st, false, 2 * L + l, 2 * F, d));
+                   gemm(EPI_RESID, L + l, 1, d, d, a, st, false));
         }
         {   // gate/up + SwiGLU
             GemmArgs a = base_args(e, M);
             a.ssq_in = ssq_at(e, l, 1);
             a.act = e->act;
             LAUNCH(SV_K_GU, l, st, gemm_bytes(2.0 * F, d, (double)M * F * 2 + (d / 128) * M * 4.0),
-                   2.0 * M * 2.0 * F * d, gemm(EPI_SWIGLU, 2 * L + l, 0, 2 * F, d, a, st, false, 3 * L + l, d, F));
+                   2.0 * M * 2.0 * F * d, gemm(EPI_SWIGLU, 2 * L + l, 0, 2 * F, d, a, st, false));
         }
         {   // down + residual (+ early-exit copy with the final gain)
             GemmArgs a = base_args(e, M);
@@ -893,7 +868,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             a.ssq_out = ssq_at(e, l + 1, 0);
             LAUNCH(SV_K_DOWN, l, st, gemm_bytes(d, F, Md * (is_exit_l ? 12 : 10) + (d / 128) * M * 4.0),
                    2.0 * M * d * F,
-                   gemm(EPI_RESID, 3 * L + l, 2, d, F, a, st, false, l + 1 < L ? l + 1 : 4 * L, l + 1 < L ? 3 * d : V, d));
+                   gemm(EPI_RESID, 3 * L + l, 2, d, F, a, st, false));
         }
         if (is_exit_l) {   // fork early exit k (S10-S11), streamed to mailbox row k
             if ((r = cudaEventRecord(e->ev_fork, st)) != cudaSuccess) return r;

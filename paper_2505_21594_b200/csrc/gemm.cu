@@ -90,7 +90,6 @@ __global__ void __launch_bounds__(128, 1)
     uint64_t* empty = full + C::STAGES;
     uint64_t* done = empty + C::STAGES;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-    int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
     float* sR = reinterpret_cast<float*>(aux + 256);          // [TN]
     float* sRed = sR + 256;                                   // [4][EPI_CHUNK]
     float* sRedDry = reinterpret_cast<float*>(aux + 2048);    // [4][EPI_CHUNK] (warm-up pass)
@@ -141,8 +140,6 @@ __global__ void __launch_bounds__(128, 1)
             mbar_arrive_expect_tx(&full[i], stage_tx);
             tma_load_2d(&tmA, sA + i * A_STAGE, &full[i], (kb0 + i) * BK, n0, pol_w);
         }
-        if (a.l2_rest)   // the rest of this CTA's weight slice -> L2 (GemmArgs::l2_rest)
-            for (int i = pre; i < nk; ++i) tma_prefetch_l2_2d(&tmA, (kb0 + i) * BK, n0);
         pdl_wait();
         gphase_mark(gtr, a.ktrace_id, 1);
         for (int i = 0; i < pre; ++i) tma_load_2d(&tmB, sB + i * C::B_STAGE, &full[i], (kb0 + i) * BK, m0 + a.b_row0, pol_x);
@@ -152,16 +149,6 @@ __global__ void __launch_bounds__(128, 1)
             mbar_arrive_expect_tx(&full[s], stage_tx);
             tma_load_2d(&tmA, sA + s * A_STAGE, &full[s], (kb0 + i) * BK, n0, pol_w);
             tma_load_2d(&tmB, sB + s * C::B_STAGE, &full[s], (kb0 + i) * BK, m0 + a.b_row0, pol_x);
-        }
-        if (a.pf_map) {   // next GEMM's first K blocks -> L2 (GemmArgs::pf_map)
-            const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-            const int ncta = gridDim.x * gridDim.y * gridDim.z;
-            for (int c = cta; c < a.pf_tiles * a.pf_splits; c += ncta) {
-                const int tile = c % a.pf_tiles, sp = c / a.pf_tiles;
-                const int k0 = (int)((long long)a.pf_kb * sp / a.pf_splits);
-                const int k1 = min((int)((long long)a.pf_kb * (sp + 1) / a.pf_splits), k0 + a.pf_depth);
-                for (int k = k0; k < k1; ++k) tma_prefetch_l2_2d(a.pf_map, k * BK, tile * TM);
-            }
         }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer (single thread)
@@ -236,8 +223,17 @@ __global__ void __launch_bounds__(128, 1)
             gphase_mark(gtr, a.ktrace_id, 2);
         }
 
+        // split-K: every split but 0 stores its partial as (value, tag) pairs with single
+        // 64-bit relaxed stores and is done; split 0 adds the others' pairs to its own
+        // partial (TMEM) in split order 0..S-1 (deterministic), polling until they carry
+        // this launch's tag (host step epoch, launch index): no fence, no ticket, one
+        // round trip when the partials are already there.  One epilogue call site, so
+        // the tail's code is small (it runs cold once per CTA).
+        const bool writer = !direct && split != 0 && !dry;
+        const size_t sstride = (size_t)NT * a.MP * TM;
         for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
             if (m0 + c0 >= a.M) break;                       // CTA-uniform
+            const int nv = min(EPI_CHUNK, a.M - (m0 + c0));
             uint32_t r[16];
             if (!dry) {
                 tmem_ld_32x32b_x16(tbase + c0, r);
@@ -246,168 +242,61 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) r[j] = 0u;
             }
-            if (direct) {
-                bar();                                       // sR visible / previous chunk consumed
-                if (!dry)
+            if (writer) {
+                uint64_t* wsp = reinterpret_cast<uint64_t*>(a.ws) + (((size_t)split * NT + nt) * a.MP + m0 + c0) * TM + row;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) sOut[j * TM + row] = __uint_as_float(r[j]);
-                bar();
-                epi_apply<EPI>(a, sOut, sR, sRedP, m0 + c0, m0, n0, nt, row, bar, kStageMeta ? sPos : nullptr,
-                               kStageMeta ? sBlk : nullptr, kPre ? &pre : nullptr, dry);
-            } else if (!dry && a.sk_tagged) {
-                if (split != 0) {   // split 0 keeps its partial in TMEM and reduces
-                    uint64_t* wsp = reinterpret_cast<uint64_t*>(a.ws) + (((size_t)split * NT + nt) * a.MP) * TM;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int tok = m0 + c0 + j;
-                        if (tok < a.M) st_relaxed_b64(&wsp[(size_t)tok * TM + row], ((uint64_t)tag << 32) | r[j]);
-                    }
-                }
-            } else if (!dry) {
-                float* wsp = a.ws + (((size_t)split * NT + nt) * a.MP) * TM;
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int tok = m0 + c0 + j;
-                    if (tok < a.M) __stcg(&wsp[(size_t)tok * TM + row], __uint_as_float(r[j]));
-                }
+                for (int j = 0; j < 16; ++j)
+                    if (j < nv) st_relaxed_b64(&wsp[(size_t)j * TM], ((uint64_t)tag << 32) | r[j]);
+                continue;
             }
-        }
-        if (direct) continue;
-
-        if (a.sk_tagged) {
-            // ---------------- split-K, tagged partials: every split but 0 stores (value,
-            // tag) pairs with single 64-bit relaxed stores and is done; split 0 reloads its
-            // own partial from TMEM and polls the others' pairs until they carry this
-            // launch's tag (step epoch, launch index): no fence, no ticket, one round trip
-            // when the partials are already there.  Sum in split order 0..S-1 (the same
-            // arithmetic as the ticketed path: deterministic).
-            if (split != 0 && !dry) continue;
-            if (!dry) gphase_mark(gtr, a.ktrace_id, 4);
-            const size_t sstride = (size_t)NT * a.MP * TM;
-            for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
-                if (m0 + c0 >= a.M) break;
-                const int nv = min(EPI_CHUNK, a.M - (m0 + c0));
-                float acc[EPI_CHUNK];
-                {
-                    uint32_t r[16];
-                    if (!dry) {
-                        tmem_ld_32x32b_x16(tbase + c0, r);
-                        tmem_ld_wait();
-                    }
+            // the chunk's fp32 tile goes through sOut[token][row]; each thread owns its
+            // row's column, so the split-K accumulation below needs no barrier
+            bar();                                           // sR visible / previous chunk consumed
+            if (!dry)
 #pragma unroll
-                    for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = dry ? 0.f : 0.f + __uint_as_float(r[j]);
-                }
+                for (int j = 0; j < EPI_CHUNK; ++j)
+                    sOut[j * TM + row] = direct ? __uint_as_float(r[j]) : 0.f + __uint_as_float(r[j]);
+            if (!direct) {
                 const uint64_t* base = reinterpret_cast<const uint64_t*>(a.ws) + ((size_t)nt * a.MP + m0 + c0) * TM + row;
-#pragma unroll
-                for (int g = 0; g < 2; ++g) {         // 8 tokens x 7 splits per round trip
-                    if (g * 8 >= nv) break;
+#pragma unroll 1
+                for (int g = 0; g * 8 < nv; ++g) {    // 8 tokens x 7 splits per round trip
                     uint64_t x[7][8];
-#pragma unroll
-                    for (int u = 0; u < 7; ++u)
-#pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            x[u][j] = (u + 1 < a.splits && g * 8 + j < nv)
-                                          ? ld_relaxed_b64(base + (u + 1) * sstride + (g * 8 + j) * TM)
-                                          : ((uint64_t)tag << 32);
-                    if (!dry) {
-                        uint32_t n = 0;
-                        for (;;) {   // re-load the pairs that do not carry this launch's tag yet
-                            bool ok = true;
-#pragma unroll
-                            for (int u = 0; u < 7; ++u)
-#pragma unroll
-                                for (int j = 0; j < 8; ++j)
-                                    if ((uint32_t)(x[u][j] >> 32) != tag) {
-                                        ok = false;
-                                        x[u][j] = ld_relaxed_b64(base + (u + 1) * sstride + (g * 8 + j) * TM);
-                                    }
-                            if (ok) break;
-                            if (++n > SV_SPIN_LIMIT) __trap();
-                        }
-                    }
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
+                    bool ok;
+                    uint32_t n = 0;
+                    do {   // all pairs in flight; again (L2 hits) until every pair carries this launch's tag
+                        ok = true;
 #pragma unroll
                         for (int u = 0; u < 7; ++u)
-                            if (u + 1 < a.splits && g * 8 + j < nv) acc[g * 8 + j] += __uint_as_float((uint32_t)x[u][j]);
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const bool live = u + 1 < a.splits && g * 8 + j < nv;
+                                x[u][j] = live ? ld_relaxed_b64(base + (u + 1) * sstride + (g * 8 + j) * TM)
+                                               : ((uint64_t)tag << 32);
+                            }
+#pragma unroll
+                        for (int u = 0; u < 7; ++u)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) ok = ok && (uint32_t)(x[u][j] >> 32) == tag;
+                        if (dry) break;
+                        if (++n > SV_SPIN_LIMIT) __trap();
+                    } while (!ok);
+                    if (dry) continue;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float v = sOut[(g * 8 + j) * TM + row];
+#pragma unroll
+                        for (int u = 0; u < 7; ++u)
+                            if (u + 1 < a.splits && g * 8 + j < nv) v += __uint_as_float((uint32_t)x[u][j]);
+                        sOut[(g * 8 + j) * TM + row] = v;
+                    }
                 }
                 if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 7);
-                bar();
-                if (!dry)
-#pragma unroll
-                    for (int j = 0; j < EPI_CHUNK; ++j) sOut[j * TM + row] = acc[j];
-                bar();
-                if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 8);
-                epi_apply<EPI>(a, sOut, sR, sRedP, m0 + c0, m0, n0, nt, row, bar, kStageMeta ? sPos : nullptr,
-                               kStageMeta ? sBlk : nullptr, kPre ? &pre : nullptr, dry);
-                if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 9);
             }
-            if (!dry) gphase_mark(gtr, a.ktrace_id, 6);
-            continue;
-        }
-
-        // ---------------- split-K through global memory: the last CTA of the tile
-        // (atomic ticket) adds the partials in split order (deterministic; measured
-        // faster at batch 1 than a cluster DSMEM reduction: C2 3.22 vs 3.34 ms)
-        // CTA barrier + one acq_rel ticket by thread 0 (release covers the CTA's
-        // partial stores through the barrier; acquire for the reducer's loads)
-        bar();
-        if (!dry && threadIdx.x == 0) *s_flag = (atomic_add_acq_rel(&a.counters[nt * MT + mt], 1) == a.splits - 1);
-        if (!dry) gphase_mark(gtr, a.ktrace_id, 3);
-        bar();
-        if (dry || *s_flag) {
-            if (!dry) gphase_mark(gtr, a.ktrace_id, 4);
-            const size_t sstride = (size_t)NT * a.MP * TM;
-            for (int c0 = 0; c0 < TN; c0 += EPI_CHUNK) {
-                if (m0 + c0 >= a.M) break;
-                const int nv = min(EPI_CHUNK, a.M - (m0 + c0));
-                float acc[EPI_CHUNK];
-#pragma unroll
-                for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = 0.f;
-                const float* base = a.ws + ((size_t)nt * a.MP + m0 + c0) * TM + row;
-                int q = 0;
-                if (nv <= 8 && a.splits <= 8) {   // batch-1 verify (<= 8 rows, <= 8 splits): one round trip
-                    float v[8][8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-#pragma unroll
-                        for (int u = 0; u < 8; ++u)
-                            v[j][u] = (j < nv && u < a.splits) ? __ldcg(base + u * sstride + j * TM) : 0.f;
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-#pragma unroll
-                        for (int u = 0; u < 8; ++u)
-                            if (u < a.splits) acc[j] += v[j][u];   // split order, as below
-                    q = a.splits;
-                }
-                for (; q + 4 <= a.splits; q += 4) {
-                    float v[EPI_CHUNK][4];
-#pragma unroll
-                    for (int j = 0; j < EPI_CHUNK; ++j)
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) v[j][u] = (j < nv) ? __ldcg(base + (q + u) * sstride + j * TM) : 0.f;
-#pragma unroll
-                    for (int j = 0; j < EPI_CHUNK; ++j)
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) acc[j] += v[j][u];
-                }
-                for (; q < a.splits; ++q) {
-#pragma unroll
-                    for (int j = 0; j < EPI_CHUNK; ++j) acc[j] += (j < nv) ? __ldcg(base + q * sstride + j * TM) : 0.f;
-                }
-                if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 7);
-                bar();
-                if (!dry)
-#pragma unroll
-                    for (int j = 0; j < EPI_CHUNK; ++j) sOut[j * TM + row] = acc[j];
-                bar();
-                if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 8);
-                epi_apply<EPI>(a, sOut, sR, sRedP, m0 + c0, m0, n0, nt, row, bar, kStageMeta ? sPos : nullptr,
-                               kStageMeta ? sBlk : nullptr, kPre ? &pre : nullptr, dry);
-                if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 9);
-            }
-            if (!dry && threadIdx.x == 0) a.counters[nt * MT + mt] = 0;
-            if (!dry) gphase_mark(gtr, a.ktrace_id, 6);
+            bar();
+            if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 8);
+            epi_apply<EPI>(a, sOut, sR, sRedP, m0 + c0, m0, n0, nt, row, bar, kStageMeta ? sPos : nullptr,
+                           kStageMeta ? sBlk : nullptr, kPre ? &pre : nullptr, dry);
+            if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 9);
         }
     }
     tc_fence_before();
@@ -447,20 +336,14 @@ int gemm_pick_tile_n(int M) {
     return 256;
 }
 
-// Split-K factor: a power of two <= 8 (env SV_SPLIT_ANY: any count <= 16),
-// only for small token tiles (TN <= 64; larger tiles have enough tiles to fill
-// the GPU), with all CTAs resident in one wave (2 per SM) and >= 2 K blocks each.
-bool g_split_any = false;     // allow non-power-of-two split counts (env SV_SPLIT_ANY)
-
+// Split-K factor: a power of two <= 8, only for small token tiles (TN <= 64; larger
+// tiles have enough tiles to fill the GPU), with all CTAs resident in one wave
+// (2 per SM) and >= 2 K blocks each.  (Non-power-of-two counts measured no gain.)
 int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms) {
     const int ntiles = (N / TM) * ((M + tile_n - 1) / tile_n);
     const int slots = num_sms * (tile_n <= 64 ? SV_GEMM_CTAS_PER_SM : 1);
     const int KB = K / BK;
     int s = 1;
-    if (g_split_any) {
-        while (s < 16 && ntiles * (s + 1) <= slots && 2 * (s + 1) <= KB) ++s;
-        return s;
-    }
     while (s < 8 && ntiles * (2 * s) <= slots && 2 * (2 * s) <= KB) s *= 2;
     return s;
 }
@@ -529,9 +412,6 @@ cudaError_t gemm_big_launch(int epi, int tile_n, const CUtensorMap& tmA, const C
 
 cudaError_t gemm_launch(int epi, int tile_n, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                         cudaStream_t st) {
-    // small-ring variant of the 16-token residual GEMM (GemmArgs::small_ring): 4 stages
-    // (76 KB), so the O projection's CTAs fit beside two attention CTAs
-    if (tile_n == 16 && epi == EPI_RESID && a.small_ring) return launch_t<16, EPI_RESID, 4>(tmA, tmB, a, st);
     // large token tiles without split-K: persistent kernel with overlapped epilogue
     if (tile_n >= 128 && a.splits == 1 && !getenv("SV_NO_BIG_GEMM")) return gemm_big_launch(epi, tile_n, tmA, tmB, a, st);
     switch (tile_n) {

@@ -34,8 +34,8 @@ struct GemmArgs {
     int splits;          // split-K factor (deterministic reduction, fixed order)
     int b_row0;          // first row of the activation tensor map (exit slot k: k * MP)
     int b_box;           // rows of the activation TMA box (<= tile_n; 0 = tile_n), M <= tile_n only
-    float* ws;           // split-K partials [splits][ntiles][MP][128] (8 bytes per element)
-    int* counters;       // [ntiles * mtiles], zero on entry, reset by the reducer
+    float* ws;           // split-K partials [splits][ntiles][MP][128] as (value, tag) 64-bit pairs
+    int* counters;       // unused by the GEMMs (kept for the argument layout)
     // RMSNorm folding: rstd[m] = 1/sqrt(sum_t ssq_in[t][m] / d + eps)
     const float* ssq_in;  // [ssq_tiles][MP] or nullptr (no scaling)
     int ssq_tiles;
@@ -59,18 +59,8 @@ struct GemmArgs {
     int d_ff;
     // EPI_LOGITS
     float* logits;        // [M][N]
-    // L2 prefetch of the next GEMM's weights: the first pf_depth K blocks of every
-    // CTA of the next launch (pf_tiles x pf_splits CTAs, pf_kb K blocks split evenly),
-    // issued once this CTA's own loads are in flight, so HBM keeps streaming through
-    // this grid's tail, the launch gap and the next grid's ramp-up.
-    const CUtensorMap* pf_map = nullptr;    // device copy of the next weight map, or nullptr
-    int pf_tiles = 0, pf_splits = 1, pf_kb = 0, pf_depth = 0;
     unsigned long long* gtrace = nullptr;   // optional phase stamps [launch][16][2] (SV_GTRACE)
     int warm = 0;         // gemm_kernel: warps 2-3 run the tail once as a dry pass (instruction-cache warm-up)
-    // the CTA's weight K blocks beyond its smem ring -> L2 before griddepcontrol.wait
-    int l2_rest = 0;
-    int small_ring = 0;   // 16-token EPI_RESID: 4-stage ring (co-resides with two attention CTAs)
-    int sk_tagged = 0;    // split-K: partials as (value, tag) pairs, split 0 reduces (else: atomic ticket)
     unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
     int ktrace_id = 0;
 };
@@ -80,7 +70,6 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 
 int gemm_pick_tile_n(int M);
 int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms);
-extern bool g_split_any;
 cudaError_t gemm_launch(int epi, int tile_n, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                         cudaStream_t st);
 
