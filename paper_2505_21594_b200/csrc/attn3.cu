@@ -16,8 +16,8 @@
 //   k-steps), causal mask, online softmax in the log2 domain on the accumulator
 //   fragments, P (bf16, straight from the S fragments) times V via ldmatrix.trans;
 // * the 4 warps' (m, l, O) are merged through shared memory in warp order, the
-//   splits of a (b, h) (one thread-block cluster) through distributed shared
-//   memory in rank order -> deterministic.
+//   splits of a (b, h) through global memory as tagged (value, tag) pairs, summed
+//   in split order -> deterministic.
 // Numerics: q and p are rounded to bf16 for the MMA (as in a bf16 model); scores,
 // softmax statistics and O accumulate in fp32.
 #include <cfloat>
@@ -68,22 +68,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
 }
-__device__ __forceinline__ uint32_t cluster_rank3() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync3() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ float ld_dsmem3(const void* p, uint32_t rank) {
-    uint32_t ra;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
-    float v;
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
-    return v;
-}
-
 #define A3_STAMP(k)                                                                                   \
     if (a.atrace && threadIdx.x == 0 && blockIdx.x == 0 && (blockIdx.y == 0 || blockIdx.y == gridDim.y - 1)) { \
         unsigned long long _t;                                                                        \
@@ -343,18 +327,47 @@ __global__ void __launch_bounds__(128, MINB) attn3_kernel(const __grid_constant_
         ktrace_mark(a.ktrace, a.ktrace_id, 1);
         return;
     }
-    cluster_sync3();                                           // split partials visible cluster-wide
-    A3_STAMP(6);
-    {   // every rank merges a slice of the G x 128 outputs (rank order of the sum: deterministic)
-        const int rk = (int)cluster_rank3();
-        for (int i = rk * 128 + tid; i < Gb * A3_D; i += S * 128) {
+    {   // ---- the splits of (b, h) through global memory as (value, tag) pairs: every
+        // split stores its (m, l, O) with single 64-bit relaxed stores (no fence), then
+        // merges a 1/S slice of the G x 128 outputs, polling the S partials of its
+        // elements until they carry this launch's tag; sum in split order 0..S-1
+        // (deterministic).  No cluster: the CTAs need not be co-scheduled.
+        const uint32_t tag = (*a.epoch << 10) | (uint32_t)(a.launch_id & 1023);
+        const size_t pstride = 16 * A3_D + 32;                // pairs per split partial
+        uint64_t* mine = a.part + ((size_t)bh * S + r) * pstride;
+        for (int i = tid; i < Gb * A3_D; i += 128) st_relaxed_b64(&mine[i], ((uint64_t)tag << 32) | __float_as_uint(fO[i]));
+        if (tid < Gb) {
+            st_relaxed_b64(&mine[16 * A3_D + 2 * tid], ((uint64_t)tag << 32) | __float_as_uint(fM[tid]));
+            st_relaxed_b64(&mine[16 * A3_D + 2 * tid + 1], ((uint64_t)tag << 32) | __float_as_uint(fL[tid]));
+        }
+        A3_STAMP(6);
+        const uint64_t* all = a.part + (size_t)bh * S * pstride;
+        for (int i = r * 128 + tid; i < Gb * A3_D; i += S * 128) {
             const int j = i / A3_D, d = i % A3_D;
+            uint64_t xm[8], xl[8], xo[8];
+            bool ok;
+            uint32_t n = 0;
+            do {   // all 3 x S pairs in flight; again (L2 hits) until all are tagged
+                ok = true;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint64_t* pq = all + (size_t)q * pstride;
+                    xm[q] = q < S ? ld_relaxed_b64(&pq[16 * A3_D + 2 * j]) : ((uint64_t)tag << 32);
+                    xl[q] = q < S ? ld_relaxed_b64(&pq[16 * A3_D + 2 * j + 1]) : ((uint64_t)tag << 32);
+                    xo[q] = q < S ? ld_relaxed_b64(&pq[j * A3_D + d]) : ((uint64_t)tag << 32);
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    ok = ok && (uint32_t)(xm[q] >> 32) == tag && (uint32_t)(xl[q] >> 32) == tag &&
+                         (uint32_t)(xo[q] >> 32) == tag;
+                if (++n > SV_SPIN_LIMIT) __trap();
+            } while (!ok);
             float mq[8], lq[8], oq[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                mq[q] = q < S ? ld_dsmem3(&fM[j], q) : -INFINITY;
-                lq[q] = q < S ? ld_dsmem3(&fL[j], q) : 0.f;
-                oq[q] = q < S ? ld_dsmem3(&fO[j * A3_D + d], q) : 0.f;
+                mq[q] = q < S ? __uint_as_float((uint32_t)xm[q]) : -INFINITY;
+                lq[q] = q < S ? __uint_as_float((uint32_t)xl[q]) : 0.f;
+                oq[q] = q < S ? __uint_as_float((uint32_t)xo[q]) : 0.f;
             }
             float M = -INFINITY;
 #pragma unroll
@@ -371,7 +384,6 @@ __global__ void __launch_bounds__(128, MINB) attn3_kernel(const __grid_constant_
                 __float2bfloat16_rn(O / L);
         }
     }
-    cluster_sync3();                                           // keep partials alive until merged
     ktrace_mark(a.ktrace, a.ktrace_id, 1);
     A3_STAMP(7);
 }
@@ -411,11 +423,13 @@ static cudaError_t attn3_launch_t(const AttnArgs& a, int splits, cudaStream_t st
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     int na = 0;
-    at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = splits;
-    at[na].val.clusterDim.y = 1;
-    at[na].val.clusterDim.z = 1;
-    ++na;
+    if (a.cluster_launch) {   // the splits of (b, h) co-scheduled as one cluster (placement only)
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = splits;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = 1;
+        ++na;
+    }
     if (g_use_pdl) {
         at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[na].val.programmaticStreamSerializationAllowed = 1;

@@ -223,6 +223,7 @@ struct sv_engine {
     bool no_t160 = false;                       // env SV_NO_T160: no 160-token persistent tiles
     bool no_wave = false;                       // env SV_NO_WAVE: always 256-token tiles above 128 rows
     bool no_warm = false;                       // env SV_NO_WARM: no instruction-cache warm-up pass in gemm_kernel
+    bool attn_no_cluster = false;               // env SV_ATTN_NO_CLUSTER: attn3 splits not launched as clusters
     int attn_pf = 0;                            // attention prefetches the O weights to L2 (env SV_ATTN_PF=1 after
                                                 // griddepcontrol.wait, 2 before it)
     int attn_splits = 0;                        // attention split override (env SV_ATTN_SPLITS; 0 = attn3_splits)
@@ -252,6 +253,8 @@ struct sv_engine {
     } pf;
     // device scratch
     float *h, *qbuf, *ssq, *logits_exit, *logits_final, *ws_main, *ws_exit, *rope, *attn_o, *attn_ml;
+    uint64_t* a3_part = nullptr;                // attn3 split partials (tagged pairs), a3_part_bh (b, h) units
+    int a3_part_bh = 0;
     bf16_raw_t *u, *u_exit, *attn_out, *act;
     int *cnt_main, *cnt_exit, *cnt_attn, *cnt_acc_exit, *cnt_acc_final;
     RowStat *stats_exit, *stats_final;
@@ -341,6 +344,10 @@ static sv_status engine_alloc(sv_engine* e) {
     CK(dalloc((void**)&e->attn_o, bh * e->max_nchunk * G * e->D * 4));
     CK(dalloc((void**)&e->attn_ml, bh * e->max_nchunk * G * 2 * 4));
     CK(dalloc((void**)&e->cnt_attn, bh * 4));
+    if (e->D == 128) {   // attn3 splits > 1 only at small batch (attn3_splits): room for 8 requests' heads
+        e->a3_part_bh = std::min(e->max_vreq, 8) * e->H;
+        CK(dalloc((void**)&e->a3_part, (size_t)e->a3_part_bh * 8 * (16 * 128 + 32) * 8));
+    }
     // acceptance
     e->acc_nch = accept_chunks(V, &e->acc_chunk);
     CK(dalloc((void**)&e->stats_exit, (size_t)e->max_rows * e->acc_nch * sizeof(RowStat)));
@@ -461,6 +468,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (getenv("SV_NO_BOX")) e->no_box = true;
     if (getenv("SV_NO_WAVE")) e->no_wave = true;
     if (getenv("SV_NO_WARM")) e->no_warm = true;
+    if (getenv("SV_ATTN_NO_CLUSTER")) e->attn_no_cluster = true;
     if (getenv("SV_NO_T160")) e->no_t160 = true;
     if (const char* ap = getenv("SV_ATTN_PF")) e->attn_pf = atoi(ap);
     e->embed = w->embed; e->lm_head = w->lm_head; e->norm_final = w->norm_final;
@@ -545,7 +553,8 @@ extern "C" sv_status sv_engine_destroy(sv_engine* e) {
                    e->attn_o, e->attn_ml, e->u, e->u_exit, e->attn_out, e->act, e->cnt_main, e->cnt_exit,
                    e->cnt_attn, e->cnt_acc_exit, e->cnt_acc_final, e->stats_exit, e->stats_final, e->race_exit,
                    e->race_final, e->res_exit_dev, e->res_final_dev, e->meta_dev, e->probs_stage,
-                   e->h_exit, e->ssq_ad, e->act_ad, e->u_ad, e->stamps_dev, e->ktrace_buf, e->atrace, e->gtrace};
+                   e->h_exit, e->ssq_ad, e->act_ad, e->u_ad, e->stamps_dev, e->ktrace_buf, e->atrace, e->gtrace,
+                   e->a3_part};
     for (void* p : dev)
         if (p) cudaFree(p);
     cudaFreeHost(e->meta_host);
@@ -837,9 +846,14 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
                 aa.pf_bytes = (size_t)d * d * 2;
                 aa.pf_early = e->attn_pf == 2;
             }
+            int a3s = e->attn_splits > 0 ? e->attn_splits : attn3_splits(nA, e->H, nchunk, e->num_sms);
+            if (nA * e->H > e->a3_part_bh) a3s = 1;   // split partials must fit a3_part
+            aa.part = e->a3_part;
+            aa.epoch = (const uint32_t*)(e->meta_dev + e->off_epoch);
+            aa.launch_id = nl;
+            aa.cluster_launch = e->attn_no_cluster ? 0 : 1;
             LAUNCH(SV_K_ATTN, l, st, attn_bytes, attn_flops,
-                   e->D == 128 ? attn3_launch(aa, e->attn_splits > 0 ? e->attn_splits : attn3_splits(nA, e->H, nchunk, e->num_sms), max_ctx, st)
-                               : attn_launch(aa, st));
+                   e->D == 128 ? attn3_launch(aa, a3s, max_ctx, st) : attn_launch(aa, st));
         }
         {   // O projection + residual
             GemmArgs a = base_args(e, M);

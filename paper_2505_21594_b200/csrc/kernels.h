@@ -100,6 +100,12 @@ struct AttnArgs {
     size_t pf_bytes = 0;
     int pf_early = 0;     // issue that prefetch at kernel start (before griddepcontrol.wait)
     int num_sms = 0;      // SMs of the engine's device (occupancy choice of attn3)
+    // attn3 split partials as (value, tag) pairs [B*H][splits][16*128 + 32]; the tag is
+    // (step epoch, launch index) so no partial of another launch is ever taken
+    uint64_t* part = nullptr;
+    const uint32_t* epoch = nullptr;
+    int launch_id = 0;
+    int cluster_launch = 0;   // launch the splits of (b, h) as one thread-block cluster (placement)
 };
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t st);
 // v3 (head_dim 128): mma.sync bf16 tensor-core tiles, per-warp cp.async rings,
