@@ -257,6 +257,7 @@ struct sv_engine {
     int a3_part_bh = 0;
     bf16_raw_t *u, *u_exit, *attn_out, *act;
     int *cnt_main, *cnt_exit, *cnt_attn, *cnt_acc_exit, *cnt_acc_final;
+    uint32_t *flags_main = nullptr, *flags_exit = nullptr;   // split-K release flags
     RowStat *stats_exit, *stats_final;
     RacePart *race_exit, *race_final;
     sv_exit_result *res_exit_dev, *res_final_dev;
@@ -336,6 +337,8 @@ static sv_status engine_alloc(sv_engine* e) {
     const int max_tiles = std::max({3 * d, 2 * F, V}) / 128 * (MP / 16 + 1);
     CK(dalloc((void**)&e->cnt_main, (size_t)max_tiles * 4));
     CK(dalloc((void**)&e->cnt_exit, (size_t)max_tiles * 4));
+    CK(dalloc((void**)&e->flags_main, (size_t)8 * max_tiles * 128 * 4));
+    CK(dalloc((void**)&e->flags_exit, (size_t)8 * max_tiles * 128 * 4));
     // attention partials
     e->max_nchunk = e->cfg.max_ctx / 64 + 1;
     // per-page attention partials (attn_kernel, head_dim != 128)
@@ -468,6 +471,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (getenv("SV_NO_BOX")) e->no_box = true;
     if (getenv("SV_NO_WAVE")) e->no_wave = true;
     if (getenv("SV_NO_WARM")) e->no_warm = true;
+    if (getenv("SV_SPLIT_POW2")) g_split_fill = false;
     if (getenv("SV_ATTN_NO_CLUSTER")) e->attn_no_cluster = true;
     if (getenv("SV_NO_T160")) e->no_t160 = true;
     if (const char* ap = getenv("SV_ATTN_PF")) e->attn_pf = atoi(ap);
@@ -554,7 +558,7 @@ extern "C" sv_status sv_engine_destroy(sv_engine* e) {
                    e->cnt_attn, e->cnt_acc_exit, e->cnt_acc_final, e->stats_exit, e->stats_final, e->race_exit,
                    e->race_final, e->res_exit_dev, e->res_final_dev, e->meta_dev, e->probs_stage,
                    e->h_exit, e->ssq_ad, e->act_ad, e->u_ad, e->stamps_dev, e->ktrace_buf, e->atrace, e->gtrace,
-                   e->a3_part};
+                   e->a3_part, e->flags_main, e->flags_exit};
     for (void* p : dev)
         if (p) cudaFree(p);
     cudaFreeHost(e->meta_host);
@@ -730,6 +734,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         a.K = K;
         a.ws = exit_ws ? e->ws_exit : e->ws_main;
         a.counters = exit_ws ? e->cnt_exit : e->cnt_main;
+        a.sk_flags = exit_ws ? e->flags_exit : e->flags_main;
         a.ktrace = e->ktrace;
         a.ktrace_id = nl;
         a.gtrace = e->ktrace ? e->gtrace : nullptr;

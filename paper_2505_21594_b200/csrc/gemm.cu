@@ -180,10 +180,13 @@ __global__ void __launch_bounds__(128, 1)
     const int row = warp * 32 + lane;
     const uint32_t tbase = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     const bool direct = (a.splits == 1);
+    // tiles of more than one 16-token chunk reduce split-K through fp32 partials and one
+    // release/acquire flag per (split, row); single-chunk tiles through tagged pairs
+    constexpr bool kFlags = TN > EPI_CHUNK;
     const uint32_t tag = (a.meta.epoch ? (*a.meta.epoch << 10) : 0u) | (uint32_t)(a.ktrace_id & 1023);
-    if (warp >= 2 && a.warm && kStageMeta)   // valid (zero) token metadata for the warm-up pass's loads
+    if (warp >= 2 && a.warm && TN <= 32 && kStageMeta)   // valid (zero) token metadata for the warm-up pass's loads
         for (int t = threadIdx.x - 64; t < TN; t += 64) sPos[t] = sBlk[t] = 0;
-    for (int pass = (warp >= 2 && a.warm) ? 0 : 1; pass < 2; ++pass) {
+    for (int pass = (warp >= 2 && a.warm && TN <= 32) ? 0 : 1; pass < 2; ++pass) {
         const bool dry = pass == 0;
         const EpiBar bar{dry ? 1 : 0, dry ? 64 : 128};
         float* sRedP = dry ? sRedDry : sRed;
@@ -243,10 +246,17 @@ __global__ void __launch_bounds__(128, 1)
                 for (int j = 0; j < 16; ++j) r[j] = 0u;
             }
             if (writer) {
-                uint64_t* wsp = reinterpret_cast<uint64_t*>(a.ws) + (((size_t)split * NT + nt) * a.MP + m0 + c0) * TM + row;
+                if constexpr (kFlags) {   // fp32 partial; the row's flag follows the last chunk
+                    float* wsp = a.ws + (((size_t)split * NT + nt) * a.MP + m0 + c0) * TM + row;
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (j < nv) st_relaxed_b64(&wsp[(size_t)j * TM], ((uint64_t)tag << 32) | r[j]);
+                    for (int j = 0; j < 16; ++j)
+                        if (j < nv) __stcg(&wsp[(size_t)j * TM], __uint_as_float(r[j]));
+                } else {
+                    uint64_t* wsp = reinterpret_cast<uint64_t*>(a.ws) + (((size_t)split * NT + nt) * a.MP + m0 + c0) * TM + row;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < nv) st_relaxed_b64(&wsp[(size_t)j * TM], ((uint64_t)tag << 32) | r[j]);
+                }
                 continue;
             }
             // the chunk's fp32 tile goes through sOut[token][row]; each thread owns its
@@ -256,7 +266,32 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
                 for (int j = 0; j < EPI_CHUNK; ++j)
                     sOut[j * TM + row] = direct ? __uint_as_float(r[j]) : 0.f + __uint_as_float(r[j]);
-            if (!direct) {
+            if (!direct && kFlags) {
+                // multi-chunk tile: one acquire of each writer's flag for this row (before
+                // the first chunk), then every chunk's partial loads pipeline freely
+                if (c0 == 0 && !dry)
+                    for (int u = 1; u < a.splits; ++u) {
+                        const uint32_t* f = a.sk_flags + (((size_t)u * NT + nt) * MT + mt) * TM + row;
+                        for (uint32_t n = 0; ld_acquire_u32(f) != tag; ++n)
+                            if (n > SV_SPIN_LIMIT) __trap();
+                    }
+                const float* base = a.ws + ((size_t)nt * a.MP + m0 + c0) * TM + row;
+                float acc[EPI_CHUNK];
+#pragma unroll
+                for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = 0.f + __uint_as_float(r[j]);
+#pragma unroll
+                for (int u = 1; u < 8; ++u)
+                    if (u < a.splits) {
+                        float v[EPI_CHUNK];
+#pragma unroll
+                        for (int j = 0; j < EPI_CHUNK; ++j) v[j] = j < nv ? __ldcg(base + u * sstride + j * TM) : 0.f;
+#pragma unroll
+                        for (int j = 0; j < EPI_CHUNK; ++j) acc[j] += v[j];
+                    }
+                if (!dry)
+#pragma unroll
+                    for (int j = 0; j < EPI_CHUNK; ++j) sOut[j * TM + row] = acc[j];
+            } else if (!direct) {
                 const uint64_t* base = reinterpret_cast<const uint64_t*>(a.ws) + ((size_t)nt * a.MP + m0 + c0) * TM + row;
 #pragma unroll 1
                 for (int g = 0; g * 8 < nv; ++g) {    // 8 tokens x 7 splits per round trip
@@ -298,6 +333,9 @@ __global__ void __launch_bounds__(128, 1)
                            kStageMeta ? sBlk : nullptr, kPre ? &pre : nullptr, dry);
             if (!dry && c0 == 0) gphase_mark(gtr, a.ktrace_id, 9);
         }
+        if constexpr (kFlags)
+            if (writer)   // release: this thread's partial stores of every chunk precede the flag
+                st_release_u32(a.sk_flags + (((size_t)split * NT + nt) * MT + mt) * TM + row, tag);
     }
     tc_fence_before();
     __syncthreads();
@@ -336,14 +374,21 @@ int gemm_pick_tile_n(int M) {
     return 256;
 }
 
-// Split-K factor: a power of two <= 8, only for small token tiles (TN <= 64; larger
-// tiles have enough tiles to fill the GPU), with all CTAs resident in one wave
-// (2 per SM) and >= 2 K blocks each.  (Non-power-of-two counts measured no gain.)
+// Split-K factor <= 8, only for small token tiles (TN <= 64; larger tiles have
+// enough tiles to fill the GPU), with all CTAs resident in one wave (2 per SM) and
+// >= 2 K blocks each: a power of two, or (g_split_fill) the largest count that
+// still fits the wave (QKV at batch 1: 3 splits = 288 CTAs on 296 slots).
+bool g_split_fill = true;   // env SV_SPLIT_POW2: powers of two only
+
 int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms) {
     const int ntiles = (N / TM) * ((M + tile_n - 1) / tile_n);
     const int slots = num_sms * (tile_n <= 64 ? SV_GEMM_CTAS_PER_SM : 1);
     const int KB = K / BK;
     int s = 1;
+    if (g_split_fill && tile_n <= 64) {
+        s = std::max(1, std::min({8, slots / ntiles, KB / 2}));
+        return s;
+    }
     while (s < 8 && ntiles * (2 * s) <= slots && 2 * (2 * s) <= KB) s *= 2;
     return s;
 }

@@ -36,6 +36,7 @@ struct GemmArgs {
     int b_box;           // rows of the activation TMA box (<= tile_n; 0 = tile_n), M <= tile_n only
     float* ws;           // split-K partials [splits][ntiles][MP][128] as (value, tag) 64-bit pairs
     int* counters;       // unused by the GEMMs (kept for the argument layout)
+    uint32_t* sk_flags;  // [splits][ntiles][128] release flags (tiles of more than one 16-token chunk)
     // RMSNorm folding: rstd[m] = 1/sqrt(sum_t ssq_in[t][m] / d + eps)
     const float* ssq_in;  // [ssq_tiles][MP] or nullptr (no scaling)
     int ssq_tiles;
@@ -70,6 +71,7 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
 
 int gemm_pick_tile_n(int M);
 int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms);
+extern bool g_split_fill;
 cudaError_t gemm_launch(int epi, int tile_n, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                         cudaStream_t st);
 
