@@ -223,6 +223,7 @@ struct sv_engine {
     bool no_t160 = false;                       // env SV_NO_T160: no 160-token persistent tiles
     bool no_wave = false;                       // env SV_NO_WAVE: always 256-token tiles above 128 rows
     bool no_warm = false;                       // env SV_NO_WARM: no instruction-cache warm-up pass in gemm_kernel
+    bool no_stream_k = false;                   // env SV_NO_STREAM_K: whole tiles in the persistent GEMM
     bool attn_no_cluster = false;               // env SV_ATTN_NO_CLUSTER: attn3 splits not launched as clusters
     int attn_pf = 0;                            // attention prefetches the O weights to L2 (env SV_ATTN_PF=1 after
                                                 // griddepcontrol.wait, 2 before it)
@@ -331,6 +332,7 @@ static sv_status engine_alloc(sv_engine* e) {
             if (sp > 1) ws = std::max(ws, (size_t)sp * (s[0] / 128) * MP * 128);
         }
     }
+    ws = std::max(ws, (size_t)e->num_sms * 256 * 128);   // stream-K partials [P][TN][128]
     e->ws_elems = ws;
     CK(dalloc((void**)&e->ws_main, ws * 8));   // (value, tag) pairs
     CK(dalloc((void**)&e->ws_exit, ws * 8));
@@ -471,6 +473,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (getenv("SV_NO_BOX")) e->no_box = true;
     if (getenv("SV_NO_WAVE")) e->no_wave = true;
     if (getenv("SV_NO_WARM")) e->no_warm = true;
+    if (getenv("SV_NO_STREAM_K")) e->no_stream_k = true;
     if (getenv("SV_SPLIT_POW2")) g_split_fill = false;
     if (getenv("SV_ATTN_NO_CLUSTER")) e->attn_no_cluster = true;
     if (getenv("SV_NO_T160")) e->no_t160 = true;
@@ -759,6 +762,18 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         const auto& tmal = e->tm_act[tl];
         const CUtensorMap& A = e->wmap128[wid];
         a.splits = gemm_pick_splits(N, K, M, tl, e->num_sms);
+        // stream-K on the main stream when whole tiles leave the last wave of the
+        // persistent grid under 90% full (C5: QKV 96 tiles, gate/up 172 on 148 SMs).
+        // Never on the exit stream: its reducers could wait on CTAs that cannot
+        // become resident beside a main-stream stream-K grid.
+        if (tl >= 128 && !exit_ws && !e->no_stream_k && a.M == M) {
+            const long long tiles = (long long)(N / 128) * ((M + tl - 1) / tl);
+            const long long waves = (tiles + e->num_sms - 1) / e->num_sms;
+            if ((double)tiles / (double)(waves * e->num_sms) < 0.9) {
+                a.stream_k = 1;
+                a.splits = 1;
+            }
+        }
         const CUtensorMap* Bp = &tmal[bbuf];
         if (M < tl && !e->no_box) {   // one token tile: load only its real rows
             const int box = (M + 7) / 8 * 8;

@@ -458,7 +458,8 @@ cudaError_t gemm_big_launch(int epi, int tile_n, const CUtensorMap& tmA, const C
 cudaError_t gemm_launch(int epi, int tile_n, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                         cudaStream_t st) {
     // large token tiles without split-K: persistent kernel with overlapped epilogue
-    if (tile_n >= 128 && a.splits == 1 && !getenv("SV_NO_BIG_GEMM")) return gemm_big_launch(epi, tile_n, tmA, tmB, a, st);
+    if (tile_n >= 128 && (a.splits == 1 || a.stream_k) && !getenv("SV_NO_BIG_GEMM"))
+        return gemm_big_launch(epi, tile_n, tmA, tmB, a, st);
     switch (tile_n) {
         case 16: return launch_epi<16>(epi, tmA, tmB, a, st);
         case 32: return launch_epi<32>(epi, tmA, tmB, a, st);

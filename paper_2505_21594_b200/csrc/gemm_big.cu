@@ -47,7 +47,27 @@ struct EpiBar {   // one epilogue group (named barrier 1 + group)
 };
 __device__ __forceinline__ void epi_all_bar() { asm volatile("bar.sync 3, 256;" ::: "memory"); }
 
-template <int TN, int EPI>
+// Stream-K (SK): the T x KB (tile, K block) units are dealt to the P CTAs as equal
+// contiguous ranges, so every SM streams the same number of weight bytes whatever
+// T mod P is.  A CTA's range is a sequence of pieces (tile, kb0, kb1): a piece that
+// covers its whole tile runs the normal epilogue; a piece that starts mid-tile is
+// always the first piece of its CTA's range ("writer": fp32 partial -> ws[cta],
+// then one release flag per thread); the piece holding a tile's first K block
+// ("reducer", the last piece of its CTA) adds the later pieces' partials in CTA
+// (= K) order after acquiring their flags — deterministic, and a reducer only ever
+// waits for writers, which wait for nothing (all P <= #SMs CTAs are resident).
+struct SkPiece {
+    int t, kb0, kb1;
+};
+__device__ __forceinline__ long long sk_bound(long long U, int P, int c) { return U * c / P; }
+__device__ __forceinline__ int sk_cta_of(long long u, long long U, int P) {   // CTA whose range holds unit u
+    int c = (int)((u * P) / U);
+    while (c + 1 < P && sk_bound(U, P, c + 1) <= u) ++c;
+    while (c > 0 && sk_bound(U, P, c) > u) --c;
+    return c;
+}
+
+template <int TN, int EPI, bool SK = false>
 __global__ void __launch_bounds__(GB_THREADS, 1)
     gemm_big_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ GemmArgs a) {
@@ -70,6 +90,36 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int NT = a.N / GB_TM, MT = (a.M + TN - 1) / TN, T = NT * MT;
     const int KB = a.K / GB_BK;
+    // the CTA's work: plain = whole tiles blockIdx.x, +P, ...; SK = unit range [u0, u1)
+    const int P = gridDim.x;
+    const long long U = (long long)T * KB;
+    const long long u0 = SK ? sk_bound(U, P, blockIdx.x) : 0, u1 = SK ? sk_bound(U, P, blockIdx.x + 1) : 0;
+    auto first_piece = [&](SkPiece& pc, long long& u) -> bool {
+        if (SK) {
+            u = u0;
+            if (u >= u1) return false;
+            pc.t = (int)(u / KB);
+            pc.kb0 = (int)(u % KB);
+            pc.kb1 = (int)min((long long)KB, pc.kb0 + (u1 - u));
+            return true;
+        }
+        pc.t = blockIdx.x;
+        pc.kb0 = 0;
+        pc.kb1 = KB;
+        return pc.t < T;
+    };
+    auto next_piece = [&](SkPiece& pc, long long& u) -> bool {
+        if (SK) {
+            u += pc.kb1 - pc.kb0;
+            if (u >= u1) return false;
+            pc.t = (int)(u / KB);
+            pc.kb0 = 0;
+            pc.kb1 = (int)min((long long)KB, u1 - u);
+            return true;
+        }
+        pc.t += P;
+        return pc.t < T;
+    };
     ktrace_mark(a.ktrace, a.ktrace_id, 0);
     if (warp == 8 && lane == 0) {
         tma_prefetch_desc(&tmA);
@@ -97,9 +147,11 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
             const uint32_t stage_tx = GB_A + (a.b_box ? a.b_box : TN) * GB_BK * 2;   // GemmArgs::b_box
             int it = 0;
             bool waited = false;
-            for (int t = blockIdx.x; t < T; t += gridDim.x) {
-                const int n0 = (t / MT) * GB_TM, m0 = (t % MT) * TN;
-                for (int kb = 0; kb < KB; ++kb, ++it) {
+            SkPiece pc;
+            long long u;
+            for (bool ok = first_piece(pc, u); ok; ok = next_piece(pc, u)) {
+                const int n0 = (pc.t / MT) * GB_TM, m0 = (pc.t % MT) * TN;
+                for (int kb = pc.kb0; kb < pc.kb1; ++kb, ++it) {
                     const int s = it % C::STAGES;
                     if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
                     mbar_arrive_expect_tx(&full[s], stage_tx);
@@ -116,12 +168,14 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
         if (lane == 0) {   // ------------------------------------------ MMA issuer
             constexpr uint32_t idesc = umma_idesc_bf16(GB_TM, TN);
             int it = 0, seg = 0;
-            for (int t = blockIdx.x; t < T; t += gridDim.x, ++seg) {
+            SkPiece pc;
+            long long u;
+            for (bool ok = first_piece(pc, u); ok; ok = next_piece(pc, u), ++seg) {
                 const int buf = seg & 1;
                 if (seg >= 2) mbar_wait(&tempty[buf], ((seg >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t dt = tmem + buf * TN;
-                for (int kb = 0; kb < KB; ++kb, ++it) {
+                for (int kb = pc.kb0; kb < pc.kb1; ++kb, ++it) {
                     const int s = it % C::STAGES;
                     mbar_wait(&full[s], (it / C::STAGES) & 1);
                     tc_fence_after();
@@ -129,7 +183,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                     const uint64_t bd = umma_sdesc_sw128(smem_u32(sB + s * C::B_STAGE));
 #pragma unroll
                     for (int k = 0; k < GB_BK / 16; ++k)
-                        umma_bf16(dt, ad + 2 * k, bd + 2 * k, idesc, (kb | k) ? 1u : 0u);
+                        umma_bf16(dt, ad + 2 * k, bd + 2 * k, idesc, (kb > pc.kb0 || k) ? 1u : 0u);
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[buf]);
@@ -142,27 +196,77 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
         float* sOut = sOut0 + grp * EPI_CHUNK * GB_TM;
         float* sRed = sRed0 + grp * 4 * EPI_CHUNK;
         pdl_wait();                                        // epilogue inputs come from earlier kernels
+        const uint32_t tag = SK ? ((*a.meta.epoch << 10) | (uint32_t)(a.ktrace_id & 1023)) : 0u;
         int seg = 0;
-        for (int t = blockIdx.x; t < T; t += gridDim.x, ++seg) {
+        SkPiece pc;
+        long long u;
+        for (bool ok = first_piece(pc, u); ok; ok = next_piece(pc, u), ++seg) {
             const int buf = seg & 1;
-            const int nt = t / MT, n0 = nt * GB_TM, m0 = (t % MT) * TN;
-            epi_rstd(a, sR, m0, TN, tid, 256);             // overlaps the tile's MMA
-            if constexpr (EPI == EPI_QKV) epi_meta(a, sPos, sBlk, m0, TN, tid, 256);
+            const int t = pc.t, nt = t / MT, n0 = nt * GB_TM, m0 = (t % MT) * TN;
+            const bool writer = SK && pc.kb0 > 0;                    // later K blocks of a split tile
+            const bool reducer = SK && pc.kb0 == 0 && pc.kb1 < KB;   // first K blocks: adds the others
+            const int cl = reducer ? sk_cta_of((long long)(t + 1) * KB - 1, U, P) : 0;
+            if (!writer) {
+                epi_rstd(a, sR, m0, TN, tid, 256);         // overlaps the tile's MMA
+                if constexpr (EPI == EPI_QKV) epi_meta(a, sPos, sBlk, m0, TN, tid, 256);
+            }
             epi_all_bar();
             mbar_wait(&tfull[buf], (seg >> 1) & 1);
             tc_fence_after();
             const uint32_t tb = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + buf * TN;
+            if (reducer) {   // the writers of this tile: CTAs blockIdx.x + 1 .. cl (their first pieces)
+                for (int c = blockIdx.x + 1; c <= cl; ++c) {
+                    const uint32_t* f = a.sk_flags + ((size_t)c * 2 + grp) * GB_TM + r;
+                    for (uint32_t n = 0; ld_acquire_u32(f) != tag; ++n)
+                        if (n > SV_SPIN_LIMIT) __trap();
+                }
+            }
             for (int c0 = grp * EPI_CHUNK; c0 < TN; c0 += 2 * EPI_CHUNK) {
                 if (m0 + c0 >= a.M) break;                 // uniform over the group
+                const int nv = min(EPI_CHUNK, a.M - (m0 + c0));
+                // the chunk's epilogue inputs that do not depend on the accumulator, issued
+                // with (before) the partial loads: one round trip per chunk
+                EpiPre pre;
+                if (!writer) {
+                    if constexpr (EPI == EPI_RESID) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            pre.h[j] = j < nv ? __ldcg(&a.h[(size_t)(m0 + c0 + j) * a.d_model + n0 + r]) : 0.f;
+                        pre.g = __bfloat162float(reinterpret_cast<const bf16*>(a.g_out)[n0 + r]);
+                        pre.g2 = a.u_out2 ? __bfloat162float(reinterpret_cast<const bf16*>(a.g_out2)[n0 + r]) : 0.f;
+                    }
+                }
                 uint32_t v[16];
                 tmem_ld_32x32b_x16(tb + c0, v);
                 tmem_ld_wait();
+                if (writer) {
+                    float* w = a.ws + ((size_t)blockIdx.x * TN + c0) * GB_TM + r;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < nv) __stcg(&w[(size_t)j * GB_TM], __uint_as_float(v[j]));
+                    continue;
+                }
+                float acc[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] = reducer ? 0.f + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+                if (reducer)
+                    for (int c = blockIdx.x + 1; c <= cl; ++c) {   // K order
+                        const float* w = a.ws + ((size_t)c * TN + c0) * GB_TM + r;
+                        float x[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) x[j] = j < nv ? __ldcg(&w[(size_t)j * GB_TM]) : 0.f;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) acc[j] += x[j];
+                    }
                 bar();
 #pragma unroll
-                for (int j = 0; j < 16; ++j) sOut[j * GB_TM + r] = __uint_as_float(v[j]);
+                for (int j = 0; j < 16; ++j) sOut[j * GB_TM + r] = acc[j];
                 bar();
-                epi_apply<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt, r, bar, sPos, sBlk);
+                epi_apply<EPI>(a, sOut, sR, sRed, m0 + c0, m0, n0, nt, r, bar, sPos, sBlk,
+                               EPI == EPI_RESID ? &pre : nullptr);
             }
+            if (writer)   // release: this thread's partial stores precede its flag
+                st_release_u32(a.sk_flags + ((size_t)blockIdx.x * 2 + grp) * GB_TM + r, tag);
             tc_fence_before();
             epi_all_bar();                                 // also guards sR / sPos reuse
             if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
@@ -174,13 +278,13 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
     ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 
-template <int TN, int EPI>
+template <int TN, int EPI, bool SK>
 static cudaError_t big_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a, cudaStream_t st) {
     using C = GBCfg<TN>;
     static bool attr = false;
     static int sms = 0;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_big_kernel<TN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(gemm_big_kernel<TN, EPI, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM);
         if (e != cudaSuccess) return e;
         int dev = 0;
@@ -189,8 +293,9 @@ static cudaError_t big_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const G
         attr = true;
     }
     const int T = (a.N / GB_TM) * ((a.M + TN - 1) / TN);
+    const long long U = (long long)T * (a.K / GB_BK);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(T < sms ? T : sms, 1, 1);
+    cfg.gridDim = dim3(SK ? (int)(U < sms ? U : sms) : (T < sms ? T : sms), 1, 1);
     cfg.blockDim = dim3(GB_THREADS, 1, 1);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
@@ -199,18 +304,18 @@ static cudaError_t big_t(const CUtensorMap& tmA, const CUtensorMap& tmB, const G
     attr1[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr1;
     cfg.numAttrs = g_use_pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, gemm_big_kernel<TN, EPI>, tmA, tmB, a);
+    return cudaLaunchKernelEx(&cfg, gemm_big_kernel<TN, EPI, SK>, tmA, tmB, a);
 }
 
 template <int TN>
 static cudaError_t big_epi(int epi, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                            cudaStream_t st) {
     switch (epi) {
-        case EPI_QKV: return big_t<TN, EPI_QKV>(tmA, tmB, a, st);
-        case EPI_RESID: return big_t<TN, EPI_RESID>(tmA, tmB, a, st);
-        case EPI_SWIGLU: return big_t<TN, EPI_SWIGLU>(tmA, tmB, a, st);
-        case EPI_LOGITS: return big_t<TN, EPI_LOGITS>(tmA, tmB, a, st);
-        case EPI_SILU: return big_t<TN, EPI_SILU>(tmA, tmB, a, st);
+        case EPI_QKV: return a.stream_k ? big_t<TN, EPI_QKV, true>(tmA, tmB, a, st) : big_t<TN, EPI_QKV, false>(tmA, tmB, a, st);
+        case EPI_RESID: return a.stream_k ? big_t<TN, EPI_RESID, true>(tmA, tmB, a, st) : big_t<TN, EPI_RESID, false>(tmA, tmB, a, st);
+        case EPI_SWIGLU: return a.stream_k ? big_t<TN, EPI_SWIGLU, true>(tmA, tmB, a, st) : big_t<TN, EPI_SWIGLU, false>(tmA, tmB, a, st);
+        case EPI_LOGITS: return big_t<TN, EPI_LOGITS, false>(tmA, tmB, a, st);
+        case EPI_SILU: return big_t<TN, EPI_SILU, false>(tmA, tmB, a, st);
     }
     return cudaErrorInvalidValue;
 }

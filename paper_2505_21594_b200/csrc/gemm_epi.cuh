@@ -20,6 +20,19 @@ constexpr int EPI_TM = 128;       // weight rows per tile
 constexpr int EPI_CHUNK = 16;     // token columns per epilogue pass
 constexpr int EPI_PAGE = 64;      // KV page size (sv_model_cfg.page_tokens is required to be 64)
 
+// one step of a transposing warp butterfly: lanes with bit SH set keep the upper W of
+// v[0..2W), the others the lower W, each adding the partner lane's copy of its half
+template <int W, int SH>
+__device__ __forceinline__ void butterfly_half(float* v, int lane) {
+    const bool hi = (lane & SH) != 0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        const float keep = hi ? v[i + W] : v[i];
+        const float send = hi ? v[i] : v[i + W];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, SH);
+    }
+}
+
 // Inputs of a single 16-token tile's epilogue that do not depend on the
 // accumulator, loaded by every thread while the tensor core still runs (so the
 // split-K reducer's tail has no load round trip of its own): the residual column
@@ -117,17 +130,31 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& a, const float* sOut, 
 #pragma unroll
         for (int j = 0; j < EPI_CHUNK; ++j) {
             if (j < nv) hv[j] += sOut[j * TM + r];
+#ifdef SV_EXP_NO_RESID_STORES
+            if (j < nv && !dry && a.M < 0) {
+#else
             if (j < nv && !dry) {
+#endif
                 const size_t idx = (size_t)(tok0 + j) * d + n0 + r;
                 a.h[idx] = hv[j];
                 reinterpret_cast<bf16*>(a.u_out)[idx] = __float2bfloat16_rn(hv[j] * g);
                 if (a.h_out2) a.h_out2[idx] = hv[j];
                 if (a.u_out2) reinterpret_cast<bf16*>(a.u_out2)[idx] = __float2bfloat16_rn(hv[j] * g2);
             }
-            if (j < nv) {                            // (uniform) only the live tokens' sums
-                const float sq = warp_sum(hv[j] * hv[j]);
-                if (lane == 0) sRed[warp * EPI_CHUNK + j] = sq;
-            }
+        }
+        {   // sum of h^2 over the warp's 32 rows for all 16 tokens at once: a transposing
+            // butterfly (8 + 4 + 2 + 1 + 1 independent shuffles instead of 16 x 5
+            // dependent ones); lane pairs (2t, 2t+1) end with token t's sum
+            float v[EPI_CHUNK];
+#pragma unroll
+            for (int j = 0; j < EPI_CHUNK; ++j) v[j] = hv[j] * hv[j];
+            butterfly_half<8, 16>(v, lane);
+            butterfly_half<4, 8>(v, lane);
+            butterfly_half<2, 4>(v, lane);
+            butterfly_half<1, 2>(v, lane);
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+            const int t = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+            if ((lane & 1) == 0) sRed[warp * EPI_CHUNK + t] = v[0];
         }
         sync();
         if (r < EPI_CHUNK && tok0 + r < a.M && !dry) {

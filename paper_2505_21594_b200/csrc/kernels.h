@@ -62,6 +62,7 @@ struct GemmArgs {
     float* logits;        // [M][N]
     unsigned long long* gtrace = nullptr;   // optional phase stamps [launch][16][2] (SV_GTRACE)
     int warm = 0;         // gemm_kernel: warps 2-3 run the tail once as a dry pass (instruction-cache warm-up)
+    int stream_k = 0;     // gemm_big_kernel: equal (tile, K block) ranges per CTA (main stream only)
     unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
     int ktrace_id = 0;
 };

@@ -108,8 +108,9 @@ def main():
         rows = [ln.strip().split(",") for ln in open(gpath).readlines()[1:]]
         t0ns = min(int(x[4]) for x in rows)
         kinds = ["embed", "gemm_qkv", "attention", "gemm_o", "gemm_gate_up", "gemm_down"]
-        names = ["start", "pdl_wait", "mma_done", "ticket", "reduce_beg", "end", "reduce_end", "partials", "epi_beg",
-                 "epi_end"]
+        names = ["start", "pdl_wait", "mma_done|first_full", "ticket|mma_end", "reduce_beg|flags_ok", "end",
+                 "reduce_end", "partials|flags_wait", "epi_beg|c0_acc", "epi_end|c0_sout", "c0_epi", "lp_beg",
+                 "lp_rstd", "lp_tfull", "lp_end"]
         # the final acceptance pair: accept phases at its id, row_stats at id + 1 (relative to the LM head end)
         ids = sorted({int(x[0]) for x in rows if int(x[1]) == 9})
         if ids:
