@@ -762,14 +762,15 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         const auto& tmal = e->tm_act[tl];
         const CUtensorMap& A = e->wmap128[wid];
         a.splits = gemm_pick_splits(N, K, M, tl, e->num_sms);
-        // stream-K on the main stream when whole tiles leave the last wave of the
-        // persistent grid under 90% full (C5: QKV 96 tiles, gate/up 172 on 148 SMs).
+        // stream-K on the main stream when whole tiles fill under 60% of the persistent
+        // grid's waves (C5: gate/up 172 tiles on 2 x 148, O / down 32 tiles); measured
+        // slower at 65-85% (C5 QKV 96 tiles: 36.9 vs 32.7 us; LM head 250 tiles).
         // Never on the exit stream: its reducers could wait on CTAs that cannot
         // become resident beside a main-stream stream-K grid.
         if (tl >= 128 && !exit_ws && !e->no_stream_k && a.M == M) {
             const long long tiles = (long long)(N / 128) * ((M + tl - 1) / tl);
             const long long waves = (tiles + e->num_sms - 1) / e->num_sms;
-            if ((double)tiles / (double)(waves * e->num_sms) < 0.9) {
+            if ((double)tiles / (double)(waves * e->num_sms) < 0.6) {
                 a.stream_k = 1;
                 a.splits = 1;
             }
