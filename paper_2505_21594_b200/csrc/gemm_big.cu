@@ -21,6 +21,10 @@
 
 namespace sv {
 
+#ifndef SV_GB_GROUPS
+#define SV_GB_GROUPS 3
+#endif
+constexpr int GB_GROUPS = SV_GB_GROUPS;
 constexpr int GB_BK = 64;
 constexpr int GB_TM = 128;
 constexpr int GB_A = GB_TM * GB_BK * 2;
@@ -30,7 +34,7 @@ struct GBCfg {
     static constexpr int B_STAGE = TN * GB_BK * 2;
     static constexpr int STAGE = GB_A + B_STAGE;
     // two groups x (sOut [16][128] f32 + sRed [4][16]) + sR, sPos, sBlk [TN]
-    static constexpr int EPI = 2 * (EPI_CHUNK * GB_TM * 4 + 4 * EPI_CHUNK * 4) + 3 * TN * 4;
+    static constexpr int EPI = GB_GROUPS * (EPI_CHUNK * GB_TM * 4 + 4 * EPI_CHUNK * 4) + 3 * TN * 4;
     static constexpr int AUX = 512;
     static constexpr int RAW = (227 * 1024 - 1024 - EPI - AUX) / STAGE;
     static constexpr int STAGES = RAW > 8 ? 8 : RAW;
@@ -39,13 +43,19 @@ struct GBCfg {
     static_assert(STAGES >= 3 && TCOLS <= 512, "config");
 };
 
-constexpr int GB_EPI_WARPS = 8, GB_THREADS = (GB_EPI_WARPS + 2) * 32;
+// epilogue groups of 4 warps (one TMEM lane quarter each) taking every GB_GROUPS-th
+// 16-token chunk: three groups cut the tail epilogue of a 5-chunk tile (C5) from
+// 3 to 2 chunks and keep up with the tensor core at 256-token tiles (C4)
+constexpr int GB_EPI_WARPS = 4 * GB_GROUPS, GB_THREADS = (GB_EPI_WARPS + 2) * 32;
+constexpr int GB_PROD_WARP = GB_EPI_WARPS, GB_MMA_WARP = GB_EPI_WARPS + 1;
 
 struct EpiBar {   // one epilogue group (named barrier 1 + group)
     int id;
     __device__ void operator()() const { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 };
-__device__ __forceinline__ void epi_all_bar() { asm volatile("bar.sync 3, 256;" ::: "memory"); }
+__device__ __forceinline__ void epi_all_bar() {   // all epilogue warps (barrier 15)
+    asm volatile("bar.sync 15, %0;" ::"n"(GB_EPI_WARPS * 32) : "memory");
+}
 
 // Stream-K (SK): the T x KB (tile, K block) units are dealt to the P CTAs as equal
 // contiguous ranges, so every SM streams the same number of weight bytes whatever
@@ -77,8 +87,8 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
     uint8_t* sA = smem;
     uint8_t* sB = smem + C::STAGES * GB_A;
     float* sOut0 = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE);  // 2 x [EPI_CHUNK][128]
-    float* sRed0 = sOut0 + 2 * EPI_CHUNK * GB_TM;                          // 2 x [4][EPI_CHUNK]
-    float* sR = sRed0 + 2 * 4 * EPI_CHUNK;                                 // [TN]
+    float* sRed0 = sOut0 + GB_GROUPS * EPI_CHUNK * GB_TM;                  // groups x [4][EPI_CHUNK]
+    float* sR = sRed0 + GB_GROUPS * 4 * EPI_CHUNK;                         // [TN]
     int* sPos = reinterpret_cast<int*>(sR + TN);                           // [TN]
     int* sBlk = sPos + TN;                                                 // [TN]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE + C::EPI);
@@ -121,7 +131,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
         return pc.t < T;
     };
     ktrace_mark(a.ktrace, a.ktrace_id, 0);
-    if (warp == 8 && lane == 0) {
+    if (warp == GB_PROD_WARP && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         for (int s = 0; s < C::STAGES; ++s) {
@@ -134,14 +144,14 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
         }
         fence_mbar_init();
     }
-    if (warp == 9) tmem_alloc(tmem_slot, C::TCOLS);
+    if (warp == GB_MMA_WARP) tmem_alloc(tmem_slot, C::TCOLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     pdl_launch_dependents();
 
-    if (warp == 8) {
+    if (warp == GB_PROD_WARP) {
         if (lane == 0) {   // ------------------------------------------ producer
             const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
             const uint32_t stage_tx = GB_A + (a.b_box ? a.b_box : TN) * GB_BK * 2;   // GemmArgs::b_box
@@ -164,7 +174,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                 }
             }
         }
-    } else if (warp == 9) {
+    } else if (warp == GB_MMA_WARP) {
         if (lane == 0) {   // ------------------------------------------ MMA issuer
             constexpr uint32_t idesc = umma_idesc_bf16(GB_TM, TN);
             int it = 0, seg = 0;
@@ -189,8 +199,8 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                 umma_commit(&tfull[buf]);
             }
         }
-    } else {               // ------------------------------------------ epilogue warps 0-7
-        const int grp = warp >> 2, tid = threadIdx.x;     // tid 0..255
+    } else {               // ------------------------------------------ epilogue warps
+        const int grp = warp >> 2, tid = threadIdx.x;     // tid 0 .. 32 * GB_EPI_WARPS - 1
         const EpiBar bar{1 + grp};
         const int r = tid & 127;                           // tile row (TMEM lane)
         float* sOut = sOut0 + grp * EPI_CHUNK * GB_TM;
@@ -207,8 +217,8 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
             const bool reducer = SK && pc.kb0 == 0 && pc.kb1 < KB;   // first K blocks: adds the others
             const int cl = reducer ? sk_cta_of((long long)(t + 1) * KB - 1, U, P) : 0;
             if (!writer) {
-                epi_rstd(a, sR, m0, TN, tid, 256);         // overlaps the tile's MMA
-                if constexpr (EPI == EPI_QKV) epi_meta(a, sPos, sBlk, m0, TN, tid, 256);
+                epi_rstd(a, sR, m0, TN, tid, GB_EPI_WARPS * 32);         // overlaps the tile's MMA
+                if constexpr (EPI == EPI_QKV) epi_meta(a, sPos, sBlk, m0, TN, tid, GB_EPI_WARPS * 32);
             }
             epi_all_bar();
             mbar_wait(&tfull[buf], (seg >> 1) & 1);
@@ -216,12 +226,12 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
             const uint32_t tb = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + buf * TN;
             if (reducer) {   // the writers of this tile: CTAs blockIdx.x + 1 .. cl (their first pieces)
                 for (int c = blockIdx.x + 1; c <= cl; ++c) {
-                    const uint32_t* f = a.sk_flags + ((size_t)c * 2 + grp) * GB_TM + r;
+                    const uint32_t* f = a.sk_flags + ((size_t)c * GB_GROUPS + grp) * GB_TM + r;
                     for (uint32_t n = 0; ld_acquire_u32(f) != tag; ++n)
                         if (n > SV_SPIN_LIMIT) __trap();
                 }
             }
-            for (int c0 = grp * EPI_CHUNK; c0 < TN; c0 += 2 * EPI_CHUNK) {
+            for (int c0 = grp * EPI_CHUNK; c0 < TN; c0 += GB_GROUPS * EPI_CHUNK) {
                 if (m0 + c0 >= a.M) break;                 // uniform over the group
                 const int nv = min(EPI_CHUNK, a.M - (m0 + c0));
                 // the chunk's epilogue inputs that do not depend on the accumulator, issued
@@ -266,7 +276,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                                EPI == EPI_RESID ? &pre : nullptr);
             }
             if (writer)   // release: this thread's partial stores precede its flag
-                st_release_u32(a.sk_flags + ((size_t)blockIdx.x * 2 + grp) * GB_TM + r, tag);
+                st_release_u32(a.sk_flags + ((size_t)blockIdx.x * GB_GROUPS + grp) * GB_TM + r, tag);
             tc_fence_before();
             epi_all_bar();                                 // also guards sR / sPos reuse
             if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
@@ -274,7 +284,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 9) tmem_dealloc(tmem, C::TCOLS);
+    if (warp == GB_MMA_WARP) tmem_dealloc(tmem, C::TCOLS);
     ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 

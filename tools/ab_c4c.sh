@@ -11,3 +11,5 @@ run c4_32 "--config C4 --batch 32 --steps 10 --warmup 3" X=1
 run c4_64 "--config C4 --batch 64 --steps 10 --warmup 3" X=1
 run c4_128 "--config C4 --batch 128 --steps 5 --warmup 3" X=1
 run c2 "--steps 100" X=1
+run c5prev "--config C5 --steps 20 --warmup 3" SV_LIB=$L/libsv_prev.so
+run c4_32prev "--config C4 --batch 32 --steps 10 --warmup 3" SV_LIB=$L/libsv_prev.so
