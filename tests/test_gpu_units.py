@@ -210,3 +210,62 @@ def test_argument_edge_cases(svlib):
     for s in (s1, s2, s3):
         s.close()
     eng.close()
+
+
+def test_gpu_sampler_million_trials_v512(svlib):
+    """SURVEY.md §8(c) stochastic pin at scale: 10^6 GPU acceptance trials at V = 512
+    (256 requests x 4000 rounds, fresh Philox counters per round, x_1 ~ q_1): the
+    first emitted token follows p_0 (chi-square, bins with expectation < 5 merged)
+    and x_1 is accepted at rate sum_v min(p_0, q_1) (binomial), alpha = 1e-3."""
+    import ctypes as C
+    from scipy import stats
+    from paper_2505_21594_b200 import sv
+    V, B, rounds = 512, 256, 4000
+    mc = ModelCfg(n_layers=1, d_model=128, n_heads=4, d_ff=128, vocab=V, max_ctx=256)
+    eng = sv.Engine(mc, sv.Weights(mc, seed=1), max_batch=B, max_gamma=8)
+    sessions = [eng.open_session(1000 + b, 0xDEF + 17 * b) for b in range(B)]
+    rng = np.random.default_rng(21)
+    z0 = rng.standard_normal(V) * 2.0
+    z = np.stack([z0, rng.standard_normal(V)]).astype(np.float32)
+    p0 = np.exp(z0 - z0.max()); p0 /= p0.sum()
+    q1 = np.exp(rng.standard_normal(V) * 1.5); q1 /= q1.sum()
+    q1 = q1.astype(np.float32)
+    zl = torch.from_numpy(np.broadcast_to(z, (B, 2, V)).copy()).cuda()
+    qd = torch.from_numpy(np.broadcast_to(q1[None], (B, 1, V)).copy()).cuda()
+    drafts = np.zeros((B, 1), dtype=np.int32)
+    arr = (sv.sv_verify_req * B)()
+    for b in range(B):                        # the request structs are built once, re-used every round
+        r = arr[b]
+        r.session = sessions[b].h
+        r.prefix_len = 1
+        r.pending_token = 0
+        r.gamma = 1
+        r.draft_tokens = drafts[b].ctypes.data_as(C.POINTER(C.c_int32))
+        r.draft_probs = qd[b].data_ptr()
+        r.probs_on_host = 0
+    out = (sv.sv_exit_result * B)()
+    counts = np.zeros(V)
+    acc = 0
+    qcdf = np.cumsum(q1.astype(np.float64) / q1.sum())
+    for rnd in range(1, rounds + 1):
+        drafts[:, 0] = np.minimum(np.searchsorted(qcdf, rng.random(B)), V - 1)
+        for b in range(B):
+            arr[b].round_id = rnd
+        sv.check(svlib.sv_debug_accept(eng.h, C.c_void_p(zl.data_ptr()), arr, B, out))
+        for b in range(B):
+            assert out[b].status == 0
+            counts[out[b].tokens[out[b].accepted]] += 1
+            acc += out[b].accepted
+    n = B * rounds
+    exp = n * p0
+    big = exp >= 5
+    obs = np.append(counts[big], counts[~big].sum())
+    ex = np.append(exp[big], exp[~big].sum())
+    p_chi = stats.chisquare(obs, ex).pvalue
+    alpha = np.minimum(p0, q1.astype(np.float64)).sum()
+    p_bin = stats.binomtest(acc, n, alpha).pvalue
+    print(f"{n} trials: chi-square p = {p_chi:.3f}, acceptance {acc / n:.5f} vs {alpha:.5f} (p = {p_bin:.3f})")
+    assert p_chi > 1e-3 and p_bin > 1e-3
+    for s in sessions:
+        s.close()
+    eng.close()

@@ -18,8 +18,9 @@ s3 = eng.open_session(9, 9)
 r = s3.prefill(np.arange(20) % mc.vocab, sample=True)
 print("ok", [a.emitted() for a in f], r.emitted())
 PY
-# 7B-width slice: 640 query rows (persistent GEMM with 160-token tiles, attention at two CTAs / SM)
-# and one request (8-split attention clusters at three CTAs / SM, small-tile split-K GEMMs)
+# 7B-width slice: 640 query rows (persistent GEMM), 80 rows (stream-K persistent GEMM with
+# release/acquire partial flags) and one request (tagged split-K pairs, attention split
+# partials as tagged pairs, the instruction-cache warm-up passes)
 cat > /tmp/san7b.py <<'PY'
 import sys, numpy as np, torch
 sys.path.insert(0, ".")
@@ -28,7 +29,7 @@ from workload import drafts as wd
 from workload.configs import ModelCfg
 mc = ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=320)
 W = sv.Weights(mc, seed=1)
-for B, ctx in ((128, 100), (1, 300)):
+for B, ctx in ((128, 100), (16, 200), (1, 300)):
     eng = sv.Engine(mc, W, max_batch=B, max_gamma=4, use_graphs=False)
     ss = [eng.open_session(1 + b, 5 + b) for b in range(B)]
     for b, s in enumerate(ss): s.fill_kv(ctx, kv_seed=3 + b)
