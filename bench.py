@@ -49,7 +49,7 @@ UNIT = "tokens/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4", "C5"])
@@ -474,9 +474,9 @@ def run_ours(args):
             s.fill_kv(ctx, kv_seed=1000 + rid)
         sessions.append(s)
     # independent calibrated draft sets per request, one per step until they cycle
-    # (64 at <= 16 requests per GPU, so the accepted lengths follow the workload's
-    # law rather than a few fixed draws; 8 for the 256-request pool)
-    n_sets = N_SETS if per <= 16 else 8
+    # (256 for one request, 64 at <= 16 requests per GPU, so the accepted lengths
+    # follow the workload's law rather than a few fixed draws; 8 for the larger pools)
+    n_sets = 4 * N_SETS if per == 1 else (N_SETS if per <= 16 else 8)
     sets = [build_calibrated_drafts(sv, eng, sessions, pend, ctx, gamma, args.alpha, mc.vocab,
                                     7 + 1000 * as_rank + k, rounds) for k in range(n_sets)]
     xs = [x for x, _ in sets]

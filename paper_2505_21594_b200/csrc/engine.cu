@@ -339,8 +339,8 @@ static sv_status engine_alloc(sv_engine* e) {
     const int max_tiles = std::max({3 * d, 2 * F, V}) / 128 * (MP / 16 + 1);
     CK(dalloc((void**)&e->cnt_main, (size_t)max_tiles * 4));
     CK(dalloc((void**)&e->cnt_exit, (size_t)max_tiles * 4));
-    CK(dalloc((void**)&e->flags_main, (size_t)8 * max_tiles * 128 * 4));
-    CK(dalloc((void**)&e->flags_exit, (size_t)8 * max_tiles * 128 * 4));
+    CK(dalloc((void**)&e->flags_main, (size_t)16 * max_tiles * 128 * 4));
+    CK(dalloc((void**)&e->flags_exit, (size_t)16 * max_tiles * 128 * 4));
     // attention partials
     e->max_nchunk = e->cfg.max_ctx / 64 + 1;
     // per-page attention partials (attn_kernel, head_dim != 128)

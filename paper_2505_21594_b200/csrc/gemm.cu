@@ -44,6 +44,12 @@ namespace sv {
 constexpr int BK = 64;                      // K elements per stage (one 128 B swizzle row)
 constexpr int TM = 128;                     // weight rows per tile (UMMA M)
 constexpr int A_STAGE = TM * BK * 2;        // 16 KB
+// split-K partners a reducer polls in one batch (splits <= SK_MAXP + 1): 9 splits
+// fill the 296 slots with the 32 tiles of O / down at batch 1 (288 CTAs)
+#ifndef SV_SK_MAXP
+#define SV_SK_MAXP 8
+#endif
+constexpr int SK_MAXP = SV_SK_MAXP;
 #ifndef SV_GEMM_MAX_STAGES
 #define SV_GEMM_MAX_STAGES 8
 #endif
@@ -280,7 +286,7 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
                 for (int j = 0; j < EPI_CHUNK; ++j) acc[j] = 0.f + __uint_as_float(r[j]);
 #pragma unroll
-                for (int u = 1; u < 8; ++u)
+                for (int u = 1; u <= SK_MAXP; ++u)
                     if (u < a.splits) {
                         float v[EPI_CHUNK];
 #pragma unroll
@@ -295,13 +301,13 @@ __global__ void __launch_bounds__(128, 1)
                 const uint64_t* base = reinterpret_cast<const uint64_t*>(a.ws) + ((size_t)nt * a.MP + m0 + c0) * TM + row;
 #pragma unroll 1
                 for (int g = 0; g * 8 < nv; ++g) {    // 8 tokens x 7 splits per round trip
-                    uint64_t x[7][8];
+                    uint64_t x[SK_MAXP][8];
                     bool ok;
                     uint32_t n = 0;
                     do {   // all pairs in flight; again (L2 hits) until every pair carries this launch's tag
                         ok = true;
 #pragma unroll
-                        for (int u = 0; u < 7; ++u)
+                        for (int u = 0; u < SK_MAXP; ++u)
 #pragma unroll
                             for (int j = 0; j < 8; ++j) {
                                 const bool live = u + 1 < a.splits && g * 8 + j < nv;
@@ -309,7 +315,7 @@ __global__ void __launch_bounds__(128, 1)
                                                : ((uint64_t)tag << 32);
                             }
 #pragma unroll
-                        for (int u = 0; u < 7; ++u)
+                        for (int u = 0; u < SK_MAXP; ++u)
 #pragma unroll
                             for (int j = 0; j < 8; ++j) ok = ok && (uint32_t)(x[u][j] >> 32) == tag;
                         if (dry) break;
@@ -320,7 +326,7 @@ __global__ void __launch_bounds__(128, 1)
                     for (int j = 0; j < 8; ++j) {
                         float v = sOut[(g * 8 + j) * TM + row];
 #pragma unroll
-                        for (int u = 0; u < 7; ++u)
+                        for (int u = 0; u < SK_MAXP; ++u)
                             if (u + 1 < a.splits && g * 8 + j < nv) v += __uint_as_float((uint32_t)x[u][j]);
                         sOut[(g * 8 + j) * TM + row] = v;
                     }
@@ -336,6 +342,7 @@ __global__ void __launch_bounds__(128, 1)
         if constexpr (kFlags)
             if (writer)   // release: this thread's partial stores of every chunk precede the flag
                 st_release_u32(a.sk_flags + (((size_t)split * NT + nt) * MT + mt) * TM + row, tag);
+        if (dry) bar();   // the warm-up pass's smem reads end before pass 1 rewrites sR / sPos / sBlk
     }
     tc_fence_before();
     __syncthreads();
@@ -386,7 +393,7 @@ int gemm_pick_splits(int N, int K, int M, int tile_n, int num_sms) {
     const int KB = K / BK;
     int s = 1;
     if (g_split_fill && tile_n <= 64) {
-        s = std::max(1, std::min({8, slots / ntiles, KB / 2}));
+        s = std::max(1, std::min({SK_MAXP + 1, slots / ntiles, KB / 2}));
         return s;
     }
     while (s < 8 && ntiles * (2 * s) <= slots && 2 * (2 * s) <= KB) s *= 2;

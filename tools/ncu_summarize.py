@@ -20,7 +20,7 @@ def kind_of(name):
     for key, k in KIND_BY_NAME:
         if key in name:
             if k == "gemm" and "<" in name:
-                epi = name.split("<")[1].split(">")[0].split(",")[-1].strip().replace("(int)", "")
+                epi = name.split("<")[1].split(">")[0].split(",")[1].strip().replace("(int)", "")
                 return f"gemm_{GEMM_EPI.get(epi, epi)}"
             return k
     return name.split("(")[0]
