@@ -44,10 +44,10 @@ namespace sv {
 constexpr int BK = 64;                      // K elements per stage (one 128 B swizzle row)
 constexpr int TM = 128;                     // weight rows per tile (UMMA M)
 constexpr int A_STAGE = TM * BK * 2;        // 16 KB
-// split-K partners a reducer polls in one batch (splits <= SK_MAXP + 1): 9 splits
-// fill the 296 slots with the 32 tiles of O / down at batch 1 (288 CTAs)
+// split-K partners a reducer polls in one batch (splits <= SK_MAXP + 1); 9 splits
+// for O / down at batch 1 (288 CTAs) measured slower than 8 (O 10.0 vs 8.3 us)
 #ifndef SV_SK_MAXP
-#define SV_SK_MAXP 8
+#define SV_SK_MAXP 7
 #endif
 constexpr int SK_MAXP = SV_SK_MAXP;
 #ifndef SV_GEMM_MAX_STAGES

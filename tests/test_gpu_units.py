@@ -254,7 +254,7 @@ def test_gpu_sampler_million_trials_v512(svlib):
         sv.check(svlib.sv_debug_accept(eng.h, C.c_void_p(zl.data_ptr()), arr, B, out))
         for b in range(B):
             assert out[b].status == 0
-            counts[out[b].tokens[out[b].accepted]] += 1
+            counts[out[b].tokens[0]] += 1          # the first emitted token: x_1 if accepted, else the residual draw
             acc += out[b].accepted
     n = B * rounds
     exp = n * p0
