@@ -747,11 +747,15 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         // 160-token tiles (UMMA N = 160) fill the rounds of M = 640 / 1280 (C4 at 1-2 GPUs)
         int tl = tn;
         if (M > 128 && a.M == M && !e->no_wave && N < 16384) {
+            // rounds x tile rows, weighted by the tile's MMA efficiency once the GEMM is
+            // compute-bound (M >= 640): the tensor pipe is 87% busy at 256-token tiles
+            // but ~50% at 128 (C4 QKV, ncu; profiles/r02/c4_tensor_pipe.json)
             auto cost = [&](int t) {
                 const long long tiles = (long long)(N / 128) * ((M + t - 1) / t);
-                return ((tiles + e->num_sms - 1) / e->num_sms) * (long long)t;
+                const double eff = M < 640 ? 1.0 : (t >= 256 ? 1.0 : t >= 160 ? 0.92 : 0.85);
+                return (double)((tiles + e->num_sms - 1) / e->num_sms) * t / eff;
             };
-            long long best = cost(256);
+            double best = cost(256);
             tl = 256;
             if (!e->no_t160 && gemm_pick_splits(N, K, M, 160, e->num_sms) == 1 && cost(160) < best) {
                 best = cost(160);

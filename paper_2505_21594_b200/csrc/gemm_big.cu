@@ -260,13 +260,19 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) acc[j] = reducer ? 0.f + __uint_as_float(v[j]) : __uint_as_float(v[j]);
                 if (reducer)
-                    for (int c = blockIdx.x + 1; c <= cl; ++c) {   // K order
-                        const float* w = a.ws + ((size_t)c * TN + c0) * GB_TM + r;
-                        float x[16];
+                    for (int c = blockIdx.x + 1; c <= cl; c += 3) {   // K order, 3 partners' loads in flight
+                        float x[3][16];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) x[j] = j < nv ? __ldcg(&w[(size_t)j * GB_TM]) : 0.f;
+                        for (int q = 0; q < 3; ++q) {
+                            const float* w = a.ws + ((size_t)(c + q) * TN + c0) * GB_TM + r;
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) acc[j] += x[j];
+                            for (int j = 0; j < 16; ++j) x[q][j] = (j < nv && c + q <= cl) ? __ldcg(&w[(size_t)j * GB_TM]) : 0.f;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 3; ++q)
+                            if (c + q <= cl)
+#pragma unroll
+                                for (int j = 0; j < 16; ++j) acc[j] += x[q][j];
                     }
                 bar();
 #pragma unroll
