@@ -222,8 +222,10 @@ struct sv_engine {
     bool no_box = false;                        // env SV_NO_BOX: load full token tiles
     bool no_t160 = false;                       // env SV_NO_T160: no 160-token persistent tiles
     bool no_wave = false;                       // env SV_NO_WAVE: always 256-token tiles above 128 rows
+    bool no_t80 = false;                        // env SV_NO_T80: 128-token tiles for 65-80 rows
     bool no_warm = false;                       // env SV_NO_WARM: no instruction-cache warm-up pass in gemm_kernel
     bool no_stream_k = false;                   // env SV_NO_STREAM_K: whole tiles in the persistent GEMM
+    double sk_fill = 0.6;                       // env SV_SK_FILL: stream-K below this wave fill
     bool attn_no_cluster = false;               // env SV_ATTN_NO_CLUSTER: attn3 splits not launched as clusters
     int attn_pf = 0;                            // attention prefetches the O weights to L2 (env SV_ATTN_PF=1 after
                                                 // griddepcontrol.wait, 2 before it)
@@ -432,7 +434,7 @@ static sv_status engine_tmaps(sv_engine* e) {
             return fail(SV_E_DEVICE, "cuTensorMapEncodeTiled failed (weights)");
     }
     if (!make_tmap_bf16(&e->tm_lm, e->lm_head, e->V, d, 128)) return fail(SV_E_DEVICE, "tensor map (lm_head)");
-    for (int tn : {16, 32, 64, 128, 160, 256}) {
+    for (int tn : {16, 32, 64, 80, 128, 160, 256}) {
         if (tn > e->MP) continue;
         std::vector<CUtensorMap> m;
         if (!act_maps(e, tn, &m)) return fail(SV_E_DEVICE, "tensor map (activations)");
@@ -472,8 +474,10 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (const char* mb = getenv("SV_A3_MINB")) g_attn_minb = atoi(mb);
     if (getenv("SV_NO_BOX")) e->no_box = true;
     if (getenv("SV_NO_WAVE")) e->no_wave = true;
+    if (getenv("SV_NO_T80")) e->no_t80 = true;
     if (getenv("SV_NO_WARM")) e->no_warm = true;
     if (getenv("SV_NO_STREAM_K")) e->no_stream_k = true;
+    if (const char* sf = getenv("SV_SK_FILL")) e->sk_fill = atof(sf);
     if (getenv("SV_SPLIT_POW2")) g_split_fill = false;
     if (getenv("SV_ATTN_NO_CLUSTER")) e->attn_no_cluster = true;
     if (getenv("SV_NO_T160")) e->no_t160 = true;
@@ -746,6 +750,9 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         // ceil(tiles / SMs) x tile (C4 at 1 GPU: O / down 160 -> 320 tiles, 2 -> 3 rounds of half size)
         // 160-token tiles (UMMA N = 160) fill the rounds of M = 640 / 1280 (C4 at 1-2 GPUs)
         int tl = tn;
+        // 65-80 rows (C5): 80-token tiles (UMMA N = 80) — the smaller activation stage
+        // leaves room for 7 weight stages in flight instead of 6
+        if (M > 64 && M <= 80 && a.M == M && !e->no_t80) tl = 80;
         if (M > 128 && a.M == M && !e->no_wave && N < 16384) {
             // rounds x tile rows, weighted by the tile's MMA efficiency once the GEMM is
             // compute-bound (M >= 640): the tensor pipe is 87% busy at 256-token tiles
@@ -771,10 +778,10 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         // slower at 65-85% (C5 QKV 96 tiles: 36.9 vs 32.7 us; LM head 250 tiles).
         // Never on the exit stream: its reducers could wait on CTAs that cannot
         // become resident beside a main-stream stream-K grid.
-        if (tl >= 128 && !exit_ws && !e->no_stream_k && a.M == M) {
+        if (tl > 64 && !exit_ws && !e->no_stream_k && a.M == M) {
             const long long tiles = (long long)(N / 128) * ((M + tl - 1) / tl);
             const long long waves = (tiles + e->num_sms - 1) / e->num_sms;
-            if ((double)tiles / (double)(waves * e->num_sms) < 0.6) {
+            if ((double)tiles / (double)(waves * e->num_sms) < e->sk_fill) {
                 a.stream_k = 1;
                 a.splits = 1;
             }

@@ -68,7 +68,7 @@ struct GemmCfg {
         (TN <= 64 ? (228 * 1024) / SV_GEMM_CTAS_PER_SM - 1024 : 225 * 1024) - 1024 - AUX;
     static constexpr int STAGES_RAW = BUDGET / STAGE;
     static constexpr int STAGES = STAGES_RAW > MAXST ? MAXST : STAGES_RAW;
-    static constexpr int TMEM_COLS = TN < 32 ? 32 : TN;
+    static constexpr int TMEM_COLS = TN <= 32 ? 32 : TN <= 64 ? 64 : TN <= 128 ? 128 : 256;   // alloc: power of two
     static constexpr int SMEM = 1024 + STAGES * STAGE + AUX;
     static_assert(STAGES >= 2, "pipeline too shallow");
     static_assert(EPI_CHUNK * TM * 4 <= STAGES * STAGE, "epilogue tile must fit the ring");
@@ -465,12 +465,13 @@ cudaError_t gemm_big_launch(int epi, int tile_n, const CUtensorMap& tmA, const C
 cudaError_t gemm_launch(int epi, int tile_n, const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& a,
                         cudaStream_t st) {
     // large token tiles without split-K: persistent kernel with overlapped epilogue
-    if (tile_n >= 128 && (a.splits == 1 || a.stream_k) && !getenv("SV_NO_BIG_GEMM"))
+    if (tile_n > 64 && (a.splits == 1 || a.stream_k) && !getenv("SV_NO_BIG_GEMM"))
         return gemm_big_launch(epi, tile_n, tmA, tmB, a, st);
     switch (tile_n) {
         case 16: return launch_epi<16>(epi, tmA, tmB, a, st);
         case 32: return launch_epi<32>(epi, tmA, tmB, a, st);
         case 64: return launch_epi<64>(epi, tmA, tmB, a, st);
+        case 80: return launch_epi<80>(epi, tmA, tmB, a, st);
         case 128: return launch_epi<128>(epi, tmA, tmB, a, st);
         case 256: return launch_epi<256>(epi, tmA, tmB, a, st);
     }

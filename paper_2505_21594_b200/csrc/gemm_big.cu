@@ -341,6 +341,7 @@ cudaError_t gemm_big_launch(int epi, int tile_n, const CUtensorMap& tmA, const C
     if (tile_n == 128) return big_epi<128>(epi, tmA, tmB, a, st);
     if (tile_n == 256) return big_epi<256>(epi, tmA, tmB, a, st);
     if (tile_n == 160) return big_epi<160>(epi, tmA, tmB, a, st);
+    if (tile_n == 80) return big_epi<80>(epi, tmA, tmB, a, st);
     return cudaErrorInvalidValue;
 }
 
