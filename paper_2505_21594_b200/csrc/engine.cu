@@ -226,6 +226,7 @@ struct sv_engine {
     bool no_warm = false;                       // env SV_NO_WARM: no instruction-cache warm-up pass in gemm_kernel
     bool no_stream_k = false;                   // env SV_NO_STREAM_K: whole tiles in the persistent GEMM
     double sk_fill = 0.6;                       // env SV_SK_FILL: stream-K below this wave fill
+    int force_tn = 0;                           // env SV_FORCE_TN: persistent-GEMM token tile (experiments)
     bool attn_no_cluster = false;               // env SV_ATTN_NO_CLUSTER: attn3 splits not launched as clusters
     int attn_pf = 0;                            // attention prefetches the O weights to L2 (env SV_ATTN_PF=1 after
                                                 // griddepcontrol.wait, 2 before it)
@@ -478,6 +479,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (getenv("SV_NO_WARM")) e->no_warm = true;
     if (getenv("SV_NO_STREAM_K")) e->no_stream_k = true;
     if (const char* sf = getenv("SV_SK_FILL")) e->sk_fill = atof(sf);
+    if (const char* ft = getenv("SV_FORCE_TN")) e->force_tn = atoi(ft);
     if (getenv("SV_SPLIT_POW2")) g_split_fill = false;
     if (getenv("SV_ATTN_NO_CLUSTER")) e->attn_no_cluster = true;
     if (getenv("SV_NO_T160")) e->no_t160 = true;
@@ -770,7 +772,7 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             }
             if (K <= 4096 && cost(128) < best) tl = 128;   // (measured: the long-K down projection loses at 128)
         }
-        const auto& tmal = e->tm_act[tl];
+        if (e->force_tn && M > 64 && a.M == M && e->tm_act.count(e->force_tn)) tl = e->force_tn;
         const CUtensorMap& A = e->wmap128[wid];
         a.splits = gemm_pick_splits(N, K, M, tl, e->num_sms);
         // stream-K on the main stream when whole tiles fill under 60% of the persistent
@@ -786,6 +788,14 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
                 a.splits = 1;
             }
         }
+        // stream-K GEMMs with few weight tiles (O / down) at 81-160 rows: 80-token tiles —
+        // the reducing CTA's tail epilogue is half as long (measured at 160 rows, the C4
+        // 8-GPU shard: O 25.7 -> 21.5 us; QKV / gate-up, whose tiles fill the grid, lose
+        // at 80 and keep their tile)
+        if (a.stream_k && M > 80 && M <= 160 && !e->force_tn && !e->no_t80 &&
+            (long long)(N / 128) * ((M + 79) / 80) <= e->num_sms / 2)
+            tl = 80;
+        const auto& tmal = e->tm_act[tl];
         const CUtensorMap* Bp = &tmal[bbuf];
         if (M < tl && !e->no_box) {   // one token tile: load only its real rows
             const int box = (M + 7) / 8 * 8;

@@ -25,6 +25,13 @@ namespace sv {
 #define SV_GB_GROUPS 3
 #endif
 constexpr int GB_GROUPS = SV_GB_GROUPS;
+// SV_GB_TRACE (compile-time): per-launch phase stamps of the persistent GEMM in the
+// SV_GTRACE buffer (tools/trace_step.py); off in the product build
+#ifdef SV_GB_TRACE
+#define GB_MARK(ph) gphase_mark(a.gtrace, a.ktrace_id, ph)
+#else
+#define GB_MARK(ph) ((void)0)
+#endif
 constexpr int GB_BK = 64;
 constexpr int GB_TM = 128;
 constexpr int GB_A = GB_TM * GB_BK * 2;
@@ -131,6 +138,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
         return pc.t < T;
     };
     ktrace_mark(a.ktrace, a.ktrace_id, 0);
+    if (threadIdx.x == 0) GB_MARK(0);
     if (warp == GB_PROD_WARP && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
@@ -155,20 +163,33 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
         if (lane == 0) {   // ------------------------------------------ producer
             const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
             const uint32_t stage_tx = GB_A + (a.b_box ? a.b_box : TN) * GB_BK * 2;   // GemmArgs::b_box
+            // weights never depend on the previous kernel: the first ring's worth of weight
+            // blocks is requested before griddepcontrol.wait (streams during its tail)
+            int pre = 0;
+            {
+                SkPiece pc;
+                long long u;
+                for (bool ok = first_piece(pc, u); ok && pre < C::STAGES; ok = next_piece(pc, u)) {
+                    const int n0 = (pc.t / MT) * GB_TM;
+                    for (int kb = pc.kb0; kb < pc.kb1 && pre < C::STAGES; ++kb, ++pre) {
+                        mbar_arrive_expect_tx(&full[pre], stage_tx);
+                        tma_load_2d(&tmA, sA + pre * GB_A, &full[pre], kb * GB_BK, n0, pol_w);
+                    }
+                }
+            }
+            pdl_wait();
+            GB_MARK(1);
             int it = 0;
-            bool waited = false;
             SkPiece pc;
             long long u;
             for (bool ok = first_piece(pc, u); ok; ok = next_piece(pc, u)) {
                 const int n0 = (pc.t / MT) * GB_TM, m0 = (pc.t % MT) * TN;
                 for (int kb = pc.kb0; kb < pc.kb1; ++kb, ++it) {
                     const int s = it % C::STAGES;
-                    if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
-                    mbar_arrive_expect_tx(&full[s], stage_tx);
-                    tma_load_2d(&tmA, sA + s * GB_A, &full[s], kb * GB_BK, n0, pol_w);
-                    if (!waited) {     // weights above never depend on the previous kernel
-                        pdl_wait();
-                        waited = true;
+                    if (it >= pre) {
+                        if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+                        mbar_arrive_expect_tx(&full[s], stage_tx);
+                        tma_load_2d(&tmA, sA + s * GB_A, &full[s], kb * GB_BK, n0, pol_w);
                     }
                     tma_load_2d(&tmB, sB + s * C::B_STAGE, &full[s], kb * GB_BK, m0 + a.b_row0, pol_x);
                 }
@@ -188,6 +209,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                 for (int kb = pc.kb0; kb < pc.kb1; ++kb, ++it) {
                     const int s = it % C::STAGES;
                     mbar_wait(&full[s], (it / C::STAGES) & 1);
+                    if (it == 0) GB_MARK(2);
                     tc_fence_after();
                     const uint64_t ad = umma_sdesc_sw128(smem_u32(sA + s * GB_A));
                     const uint64_t bd = umma_sdesc_sw128(smem_u32(sB + s * C::B_STAGE));
@@ -198,6 +220,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                 }
                 umma_commit(&tfull[buf]);
             }
+            GB_MARK(3);
         }
     } else {               // ------------------------------------------ epilogue warps
         const int grp = warp >> 2, tid = threadIdx.x;     // tid 0 .. 32 * GB_EPI_WARPS - 1
@@ -221,7 +244,9 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                 if constexpr (EPI == EPI_QKV) epi_meta(a, sPos, sBlk, m0, TN, tid, GB_EPI_WARPS * 32);
             }
             epi_all_bar();
+            if (tid == 0) GB_MARK(11);
             mbar_wait(&tfull[buf], (seg >> 1) & 1);
+            if (tid == 0) GB_MARK(13);
             tc_fence_after();
             const uint32_t tb = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + buf * TN;
             if (reducer) {   // the writers of this tile: CTAs blockIdx.x + 1 .. cl (their first pieces)
@@ -230,6 +255,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                     for (uint32_t n = 0; ld_acquire_u32(f) != tag; ++n)
                         if (n > SV_SPIN_LIMIT) __trap();
                 }
+                if (tid == 0) GB_MARK(4);
             }
             for (int c0 = grp * EPI_CHUNK; c0 < TN; c0 += GB_GROUPS * EPI_CHUNK) {
                 if (m0 + c0 >= a.M) break;                 // uniform over the group
@@ -286,11 +312,13 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
             tc_fence_before();
             epi_all_bar();                                 // also guards sR / sPos reuse
             if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
+            if (tid == 0) GB_MARK(14);
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == GB_MMA_WARP) tmem_dealloc(tmem, C::TCOLS);
+    if (threadIdx.x == 0) GB_MARK(5);
     ktrace_mark(a.ktrace, a.ktrace_id, 1);
 }
 

@@ -284,23 +284,21 @@ def test_7b_width_two_layers(svlib):
     assert not tf.hard_mismatch and not te.hard_mismatch
 
 
-def test_7b_width_c5_batch(svlib):
-    """configs[4]-shaped batch at the Llama2-7B layer shapes (2 layers): B = 16
-    requests x (gamma + 1) = 80 query rows -> the persistent 128-token GEMM and the
-    2-stage attention ring, in bench.py's launch configuration; sampled
-    requests {0, 7, 15} against the fp64 oracle, one stochastic round."""
+def _batch_7b_against_oracle(name, B, gamma, ctx, sampled, seeds=(60, 70, 80, 33)):
+    """B requests at the Llama2-7B layer widths (2 layers), one stochastic round with an
+    early exit at layer 1: level U on every request, level E on the sampled ones."""
     from paper_2505_21594_b200 import sv
-    mc = ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=640)
-    B, gamma, ctx = 16, 4, 600
+    mc = ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=(ctx + 40 + 63) // 64 * 64)
+    s0, k0, kv0, dseed = seeds
     W = sv.Weights(mc, seed=1)
     eng = sv.Engine(mc, W, max_batch=B, max_gamma=gamma)
     model = om.Model(mc, seed=1)
     ss = []
     for b in range(B):
-        s = eng.open_session(60 + b, 70 + b)
-        s.fill_kv(ctx, kv_seed=80 + b)
+        s = eng.open_session(s0 + b, k0 + b)
+        s.fill_kv(ctx, kv_seed=kv0 + b)
         ss.append(s)
-    x, q = wd.timing_drafts(33, B, gamma, mc.vocab, s=1.1)
+    x, q = wd.timing_drafts(dseed, B, gamma, mc.vocab, s=1.1)
     qd = torch.from_numpy(q).cuda()
     t = eng.submit([sv.Request(ss[b], 1, 5 + b, x[b], qd[b]) for b in range(B)], exit_layer=1)
     early = t.wait_early()
@@ -308,26 +306,49 @@ def test_7b_width_c5_batch(svlib):
     zf = t.logits(1, gamma).cpu().numpy()
     ze = t.logits(0, gamma).cpu().numpy()
     t.release()
-    tally = Tally("7b_width_c5_batch")
-    ut = UTally("7b_width_c5_batch level U")
+    tally = Tally(name)
+    ut = UTally(name + " level U")
     for b in range(B):
-        ut.add(zf[b], final[b], x[b], q[b], (70 + b, 60 + b, 1), tag=("final", b))
-        ut.add(ze[b], early[b], x[b], q[b], (70 + b, 60 + b, 1), tag=("exit", b))
-    for b in (0, 7, 15):
-        osess = oracle_session(mc, model, 60 + b, 70 + b, 80 + b, ctx)
+        ut.add(zf[b], final[b], x[b], q[b], (k0 + b, s0 + b, 1), tag=("final", b))
+        ut.add(ze[b], early[b], x[b], q[b], (k0 + b, s0 + b, 1), tag=("exit", b))
+    for b in sampled:
+        osess = oracle_session(mc, model, s0 + b, k0 + b, kv0 + b, ctx)
         out = verify_step(model, osess, 1, 5 + b, x[b], q[b].astype(np.float64), exit_layer=1)
         rel, eps = row_rel_err(zf[b], out.final_logits)
         rel_e, eps_e = row_rel_err(ze[b], out.exit_logits)
         assert rel.max() < LOGIT_TOL and rel_e.max() < LOGIT_TOL
-        tally.add(out.final, final[b], out.final_logits, eps, q[b], (70 + b, 60 + b, 1), tag=("final", b))
-        tally.add(out.early, early[b], out.exit_logits, eps_e, q[b], (70 + b, 60 + b, 1), tag=("exit", b))
+        tally.add(out.final, final[b], out.final_logits, eps, q[b], (k0 + b, s0 + b, 1), tag=("final", b))
+        tally.add(out.early, early[b], out.exit_logits, eps_e, q[b], (k0 + b, s0 + b, 1), tag=("exit", b))
+        assert ss[b].length == final[b].new_len
     print(tally.report(), "|", ut.report())
-    save_report("7b_width_c5_batch", dict(level_e=tally.asdict(), level_u=ut.asdict()))
+    save_report(name, dict(level_e=tally.asdict(), level_u=ut.asdict()))
     assert not tally.hard_mismatch and not ut.hard_mismatch
     assert ut.checked >= 0.8 * ut.n and tally.checked >= 2
     for s in ss:
         s.close()
     eng.close()
+    return zf, ze
+
+
+def test_7b_width_c5_batch(svlib):
+    """configs[4]-shaped batch at the Llama2-7B layer shapes (2 layers): B = 16
+    requests x (gamma + 1) = 80 query rows -> the persistent GEMM (80-token tiles,
+    stream-K for QKV / O / down / gate-up: split tiles reduced by all their
+    contributors) and the attention ring, in bench.py's launch configuration; sampled
+    requests {0, 7, 15} against the fp64 oracle, one stochastic round."""
+    _batch_7b_against_oracle("7b_width_c5_batch", 16, 4, 600, (0, 7, 15))
+
+
+@pytest.mark.parametrize("sk_fill", [None, "1.01"])
+def test_7b_width_c4_shard_batch(svlib, sk_fill, monkeypatch):
+    """The per-GPU shard of configs[3] on 8 GPUs: B = 32 requests x 5 = 160 query rows
+    (160-token persistent tiles; stream-K for O / down / gate-up by default, and for
+    every GEMM with SV_SK_FILL=1.01), sampled requests {0, 17, 31} against the fp64
+    oracle; the two stream-K settings give logits within the same bound."""
+    if sk_fill:
+        monkeypatch.setenv("SV_SK_FILL", sk_fill)
+    _batch_7b_against_oracle("7b_width_c4_shard_batch" + ("_sk" if sk_fill else ""), 32, 4, 300, (0, 17, 31),
+                             seeds=(500, 600, 700, 35))
 
 
 def test_7b_width_c4_batch(svlib):
