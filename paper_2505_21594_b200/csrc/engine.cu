@@ -227,6 +227,7 @@ struct sv_engine {
     bool no_stream_k = false;                   // env SV_NO_STREAM_K: whole tiles in the persistent GEMM
     double sk_fill = 0.6;                       // env SV_SK_FILL: stream-K below this wave fill
     int force_tn = 0;                           // env SV_FORCE_TN: persistent-GEMM token tile (experiments)
+    int kv_pf_mb = -1;                          // env SV_KV_PF_MB: cached KV pulled into L2 by the QKV GEMM (-1: by rows)
     bool attn_no_cluster = false;               // env SV_ATTN_NO_CLUSTER: attn3 splits not launched as clusters
     int attn_pf = 0;                            // attention prefetches the O weights to L2 (env SV_ATTN_PF=1 after
                                                 // griddepcontrol.wait, 2 before it)
@@ -480,6 +481,7 @@ extern "C" sv_status sv_engine_create(const sv_model_cfg* cfg, const sv_weights*
     if (getenv("SV_NO_STREAM_K")) e->no_stream_k = true;
     if (const char* sf = getenv("SV_SK_FILL")) e->sk_fill = atof(sf);
     if (const char* ft = getenv("SV_FORCE_TN")) e->force_tn = atoi(ft);
+    if (const char* kp = getenv("SV_KV_PF_MB")) e->kv_pf_mb = atoi(kp);
     if (getenv("SV_SPLIT_POW2")) g_split_fill = false;
     if (getenv("SV_ATTN_NO_CLUSTER")) e->attn_no_cluster = true;
     if (getenv("SV_NO_T160")) e->no_t160 = true;
@@ -862,6 +864,14 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
             a.layer = l;
             a.ssq_in = ssq_at(e, l, 0);
             a.qbuf = e->qbuf;
+            // cached KV of this layer -> L2 during the QKV tail (measured, same box: 48 MB
+            // C5 6.68 -> 6.65 ms, C4 8-GPU shard 8.24 -> 8.14; 96 MB for C4 39.8 -> 39.4,
+            // but C5 6.81: the prefetch then overlaps C5's QKV mainloop)
+            const int kv_mb = e->kv_pf_mb >= 0 ? e->kv_pf_mb : (M >= 256 ? 96 : 48);
+            if (!pf && kv_mb > 0) {
+                a.kv_pf_B = nA;
+                a.kv_pf_blocks = (int)((double)kv_mb * (1 << 20) / (4.0 * e->H * 64 * e->D));
+            }
             LAUNCH(SV_K_QKV, l, st, gemm_bytes(3.0 * d, d, Md * 8 + (d / 128) * M * 4.0), 2.0 * M * 3.0 * d * d,
                    gemm(EPI_QKV, l, 0, 3 * d, d, a, st, false));
         }

@@ -194,6 +194,21 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                     tma_load_2d(&tmB, sB + s * C::B_STAGE, &full[s], kb * GB_BK, m0 + a.b_row0, pol_x);
                 }
             }
+            if constexpr (EPI == EPI_QKV) {   // GemmArgs::kv_pf_blocks
+                const size_t plane = (size_t)a.n_heads * EPI_PAGE * a.head_dim;   // elements per K (or V) plane
+                int item = 0;
+                for (int b = 0; b < a.kv_pf_B && item < a.kv_pf_blocks; ++b) {
+                    const int npg = (a.meta.ctx[b] + EPI_PAGE - 1) / EPI_PAGE;
+                    for (int p = 0; p < npg && item < a.kv_pf_blocks; ++p, ++item) {
+                        if (item % P != (int)blockIdx.x) continue;
+                        const int blk = a.meta.page_table[b * a.meta.pt_stride + p];
+                        const uint8_t* base = reinterpret_cast<const uint8_t*>(a.kv_pool) +
+                                              (((size_t)blk * a.n_layers + a.layer) * 2 * plane) * 2;
+                        for (size_t o = 0; o < 2 * plane * 2; o += 65536)
+                            bulk_prefetch_l2(base + o, (uint32_t)min((size_t)65536, 2 * plane * 2 - o));
+                    }
+                }
+            }
         }
     } else if (warp == GB_MMA_WARP) {
         if (lane == 0) {   // ------------------------------------------ MMA issuer

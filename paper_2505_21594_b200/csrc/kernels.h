@@ -63,6 +63,11 @@ struct GemmArgs {
     unsigned long long* gtrace = nullptr;   // optional phase stamps [launch][16][2] (SV_GTRACE)
     int warm = 0;         // gemm_kernel: warps 2-3 run the tail once as a dry pass (instruction-cache warm-up)
     int stream_k = 0;     // gemm_big_kernel: equal (tile, K block) ranges per CTA (main stream only)
+    // gemm_big_kernel, EPI_QKV: after its last weight load, each CTA pulls a share of the
+    // first kv_pf_blocks cached (request, page) KV blocks of this layer (request order,
+    // kv_pf_B requests) into L2 — the attention that follows reads them while the QKV
+    // epilogue tail leaves HBM idle
+    int kv_pf_blocks = 0, kv_pf_B = 0;
     unsigned long long* ktrace = nullptr;   // optional per-launch [first start, last end] (SV_KTRACE)
     int ktrace_id = 0;
 };
