@@ -272,6 +272,18 @@ SV_API sv_status sv_debug_logits(sv_ticket* t, int32_t which, float* dst_device)
  * sessions supply seeds / ids, nothing is committed.  Synchronous. */
 SV_API sv_status sv_debug_accept(sv_engine* e, const float* logits_dev, const sv_verify_req* reqs,
                           int32_t n, sv_exit_result* out);
+/* out[M][N] = X[M][K] . W[N][K]^T (fp32, device, row-major) through the step's
+ * tcgen05 GEMM kernels, with the token tile / split-K / stream-K choice of a step
+ * with M query rows (no folded norm, no fused epilogue).  W and X are bf16,
+ * row-major, device, 16-byte aligned; N % 128 == 0, K % 64 == 0, 1 <= M <= the
+ * engine's max rows (SV_E_INVALID otherwise; SV_E_CAPACITY when the split
+ * partials would not fit the engine's workspace).  Used to run the rank-local
+ * slices of the 8-way tensor-parallel decomposition (SURVEY.md
+ * §8(f) NEXT-4: column / row splits of W_qkv, W_o, W_gate/up, W_down, W_lm on
+ * 128-row / 64-column boundaries) on one GPU.  Synchronous; SV_E_BUSY while a
+ * ticket is in flight. */
+SV_API sv_status sv_debug_gemm(sv_engine* e, const void* w_dev, const void* x_dev, int32_t N, int32_t K, int32_t M,
+                               float* out_dev);
 /* Copy cached K and V rows first..first+count-1 of one layer to host
  * (bf16 [count][d_model], element [pos][head*head_dim + dim]).  Synchronous. */
 SV_API sv_status sv_debug_kv_rows(sv_session* s, int32_t layer, int32_t first, int32_t count,

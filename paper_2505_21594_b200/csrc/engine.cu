@@ -672,6 +672,60 @@ static float* ssq_at(sv_engine* e, int layer, int which) {   // norm point (laye
     return e->ssq + (size_t)(2 * layer + which) * (e->d / 128) * e->MP;
 }
 
+// Token tile, split-K factor and stream-K choice of one GEMM launch with M query rows
+// (a.M is the launch's row count, M the step's); sets a.splits / a.stream_k, returns
+// the token tile.  Shared by the step and the sv_debug_gemm hook.
+static int gemm_config(sv_engine* e, int M, int N, int K, bool exit_ws, GemmArgs& a) {
+    const int tn = gemm_pick_tile_n(M);
+    // persistent path (M > 128): wave-aware token tile, 128 or 256 rows, minimising
+    // ceil(tiles / SMs) x tile (C4 at 1 GPU: O / down 160 -> 320 tiles, 2 -> 3 rounds of half size)
+    // 160-token tiles (UMMA N = 160) fill the rounds of M = 640 / 1280 (C4 at 1-2 GPUs)
+    int tl = tn;
+    // 65-80 rows (C5): 80-token tiles (UMMA N = 80) — the smaller activation stage
+    // leaves room for 7 weight stages in flight instead of 6
+    if (M > 64 && M <= 80 && a.M == M && !e->no_t80) tl = 80;
+    if (M > 128 && a.M == M && !e->no_wave && N < 16384) {
+        // rounds x tile rows, weighted by the tile's MMA efficiency once the GEMM is
+        // compute-bound (M >= 640): the tensor pipe is 87% busy at 256-token tiles
+        // but ~50% at 128 (C4 QKV, ncu; profiles/r02/c4_tensor_pipe.json)
+        auto cost = [&](int t) {
+            const long long tiles = (long long)(N / 128) * ((M + t - 1) / t);
+            const double eff = M < 640 ? 1.0 : (t >= 256 ? 1.0 : t >= 160 ? 0.92 : 0.85);
+            return (double)((tiles + e->num_sms - 1) / e->num_sms) * t / eff;
+        };
+        double best = cost(256);
+        tl = 256;
+        if (!e->no_t160 && gemm_pick_splits(N, K, M, 160, e->num_sms) == 1 && cost(160) < best) {
+            best = cost(160);
+            tl = 160;
+        }
+        if (K <= 4096 && cost(128) < best) tl = 128;   // (measured: the long-K down projection loses at 128)
+    }
+    if (e->force_tn && M > 64 && a.M == M && e->tm_act.count(e->force_tn)) tl = e->force_tn;
+    a.splits = gemm_pick_splits(N, K, M, tl, e->num_sms);
+    // stream-K on the main stream when whole tiles fill under 60% of the persistent
+    // grid's waves (C5: gate/up 172 tiles on 2 x 148, O / down 32 tiles); measured
+    // slower at 65-85% (C5 QKV 96 tiles: 36.9 vs 32.7 us; LM head 250 tiles).
+    // Never on the exit stream: its reducers could wait on CTAs that cannot
+    // become resident beside a main-stream stream-K grid.
+    if (tl > 64 && !exit_ws && !e->no_stream_k && a.M == M) {
+        const long long tiles = (long long)(N / 128) * ((M + tl - 1) / tl);
+        const long long waves = (tiles + e->num_sms - 1) / e->num_sms;
+        if ((double)tiles / (double)(waves * e->num_sms) < e->sk_fill) {
+            a.stream_k = 1;
+            a.splits = 1;
+        }
+    }
+    // stream-K GEMMs with few weight tiles (O / down) at 81-160 rows: 80-token tiles —
+    // the reducing CTA's tail epilogue is half as long (measured at 160 rows, the C4
+    // 8-GPU shard: O 25.7 -> 21.5 us; QKV / gate-up, whose tiles fill the grid, lose
+    // at 80 and keep their tile)
+    if (a.stream_k && M > 80 && M <= 160 && !e->force_tn && !e->no_t80 &&
+        (long long)(N / 128) * ((M + 79) / 80) <= e->num_sms / 2)
+        tl = 80;
+    return tl;
+}
+
 // Issues every kernel / copy of one step on (main, exit) streams; returns launch count.
 // exit_mask: bit l-1 = early exit after decoder layer l; the k-th exit (ascending)
 // uses u_exit slot k, mailbox rows [k][B] and flag k (streamed as each completes).
@@ -750,53 +804,8 @@ static cudaError_t issue_step(sv_engine* e, cudaStream_t st, int n, int gamma, u
         a.ktrace_id = nl;
         a.gtrace = e->ktrace ? e->gtrace : nullptr;
         a.warm = e->no_warm ? 0 : 1;
-        // persistent path (M > 128): wave-aware token tile, 128 or 256 rows, minimising
-        // ceil(tiles / SMs) x tile (C4 at 1 GPU: O / down 160 -> 320 tiles, 2 -> 3 rounds of half size)
-        // 160-token tiles (UMMA N = 160) fill the rounds of M = 640 / 1280 (C4 at 1-2 GPUs)
-        int tl = tn;
-        // 65-80 rows (C5): 80-token tiles (UMMA N = 80) — the smaller activation stage
-        // leaves room for 7 weight stages in flight instead of 6
-        if (M > 64 && M <= 80 && a.M == M && !e->no_t80) tl = 80;
-        if (M > 128 && a.M == M && !e->no_wave && N < 16384) {
-            // rounds x tile rows, weighted by the tile's MMA efficiency once the GEMM is
-            // compute-bound (M >= 640): the tensor pipe is 87% busy at 256-token tiles
-            // but ~50% at 128 (C4 QKV, ncu; profiles/r02/c4_tensor_pipe.json)
-            auto cost = [&](int t) {
-                const long long tiles = (long long)(N / 128) * ((M + t - 1) / t);
-                const double eff = M < 640 ? 1.0 : (t >= 256 ? 1.0 : t >= 160 ? 0.92 : 0.85);
-                return (double)((tiles + e->num_sms - 1) / e->num_sms) * t / eff;
-            };
-            double best = cost(256);
-            tl = 256;
-            if (!e->no_t160 && gemm_pick_splits(N, K, M, 160, e->num_sms) == 1 && cost(160) < best) {
-                best = cost(160);
-                tl = 160;
-            }
-            if (K <= 4096 && cost(128) < best) tl = 128;   // (measured: the long-K down projection loses at 128)
-        }
-        if (e->force_tn && M > 64 && a.M == M && e->tm_act.count(e->force_tn)) tl = e->force_tn;
+        const int tl = gemm_config(e, M, N, K, exit_ws, a);
         const CUtensorMap& A = e->wmap128[wid];
-        a.splits = gemm_pick_splits(N, K, M, tl, e->num_sms);
-        // stream-K on the main stream when whole tiles fill under 60% of the persistent
-        // grid's waves (C5: gate/up 172 tiles on 2 x 148, O / down 32 tiles); measured
-        // slower at 65-85% (C5 QKV 96 tiles: 36.9 vs 32.7 us; LM head 250 tiles).
-        // Never on the exit stream: its reducers could wait on CTAs that cannot
-        // become resident beside a main-stream stream-K grid.
-        if (tl > 64 && !exit_ws && !e->no_stream_k && a.M == M) {
-            const long long tiles = (long long)(N / 128) * ((M + tl - 1) / tl);
-            const long long waves = (tiles + e->num_sms - 1) / e->num_sms;
-            if ((double)tiles / (double)(waves * e->num_sms) < e->sk_fill) {
-                a.stream_k = 1;
-                a.splits = 1;
-            }
-        }
-        // stream-K GEMMs with few weight tiles (O / down) at 81-160 rows: 80-token tiles —
-        // the reducing CTA's tail epilogue is half as long (measured at 160 rows, the C4
-        // 8-GPU shard: O 25.7 -> 21.5 us; QKV / gate-up, whose tiles fill the grid, lose
-        // at 80 and keep their tile)
-        if (a.stream_k && M > 80 && M <= 160 && !e->force_tn && !e->no_t80 &&
-            (long long)(N / 128) * ((M + 79) / 80) <= e->num_sms / 2)
-            tl = 80;
         const auto& tmal = e->tm_act[tl];
         const CUtensorMap* Bp = &tmal[bbuf];
         if (M < tl && !e->no_box) {   // one token tile: load only its real rows
@@ -1534,6 +1543,35 @@ extern "C" sv_status sv_debug_accept(sv_engine* e, const float* logits_dev, cons
     CK(accept_launch(aa, 0));
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out, e->res_final_dev, (size_t)n * sizeof(sv_exit_result), cudaMemcpyDeviceToHost));
+    return SV_OK;
+}
+
+extern "C" sv_status sv_debug_gemm(sv_engine* e, const void* w_dev, const void* x_dev, int32_t N, int32_t K, int32_t M,
+                                   float* out_dev) {
+    if (!e || !w_dev || !x_dev || !out_dev) return fail(SV_E_INVALID, "NULL argument");
+    if (N < 128 || N % 128 || K < 128 || K % 64 || M < 1 || M > e->max_rows) return fail(SV_E_INVALID, "bad shape");
+    if ((uintptr_t)w_dev % 16 || (uintptr_t)x_dev % 16) return fail(SV_E_INVALID, "operands must be 16-byte aligned");
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (e->inflight) return fail(SV_E_BUSY, "a ticket is in flight");
+    CK(cudaSetDevice(e->device));
+    GemmArgs a = base_args(e, M);
+    a.N = N;
+    a.K = K;
+    a.ssq_in = nullptr;   // no folded norm: out = X W^T
+    a.logits = out_dev;
+    a.ws = e->ws_main;
+    a.counters = e->cnt_main;
+    a.sk_flags = e->flags_main;
+    const int tl = gemm_config(e, M, N, K, false, a);
+    const size_t part = a.stream_k ? (size_t)e->num_sms * tl * 128 : (size_t)a.splits * (N / 128) * e->MP * 128;
+    if (part > e->ws_elems) return fail(SV_E_CAPACITY, "split partials exceed the engine's workspace");
+    CUtensorMap A, B;
+    if (!make_tmap_bf16(&A, w_dev, N, K, 128) || !make_tmap_bf16(&B, x_dev, M, K, tl))
+        return fail(SV_E_DEVICE, "cuTensorMapEncodeTiled failed");
+    *(uint32_t*)(e->meta_host + e->off_epoch) = ++e->epoch & 0x3FFFFF;   // fresh split-K tags
+    CK(cudaMemcpy(e->meta_dev + e->off_epoch, e->meta_host + e->off_epoch, 4, cudaMemcpyHostToDevice));
+    CK(gemm_launch(EPI_LOGITS, tl, A, B, a, 0));
+    CK(cudaDeviceSynchronize());
     return SV_OK;
 }
 

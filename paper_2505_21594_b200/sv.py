@@ -131,6 +131,7 @@ EXPORTS = {
     "sv_debug_trace_read": (C.c_int, [C.c_void_p, C.POINTER(sv_trace_rec), C.c_int32, C.POINTER(C.c_int32)]),
     "sv_debug_forward": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_void_p]),
     "sv_debug_philox": (C.c_int, [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "sv_debug_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
 }
 
 _lib = None
@@ -491,6 +492,18 @@ class Engine:
         """Exit adapters for every early exit (None: the plain shared head)."""
         self._adapters = adapters
         check(lib().sv_engine_set_adapters(self.h, C.byref(adapters.a) if adapters is not None else None))
+
+    def debug_gemm(self, w, x):
+        """out = x @ w.T (fp32) through the step's GEMM kernels; w [N, K], x [M, K] bf16
+        CUDA tensors (sv_debug_gemm: marshalling only)."""
+        import torch
+        assert w.dtype == torch.bfloat16 and x.dtype == torch.bfloat16 and w.is_cuda and x.is_cuda
+        w, x = w.contiguous(), x.contiguous()
+        N, K = w.shape
+        M = x.shape[0]
+        out = torch.empty((M, N), dtype=torch.float32, device=w.device)
+        check(lib().sv_debug_gemm(self.h, w.data_ptr(), x.data_ptr(), N, K, M, out.data_ptr()))
+        return out
 
     def last_launches(self) -> int:
         n = C.c_int32()
