@@ -5,7 +5,13 @@
 
 namespace sv {
 
-constexpr int ACC_THREADS = 256;
+// Threads per CTA: 256 when the grid is a single wave (batch 1: the race over a
+// 1024-entry chunk is ALU-latency bound, more threads per chunk finish sooner);
+// 64 (4 float4 of a chunk each) when there are more than two CTAs per SM — up to 32
+// CTAs per SM then hide the per-chunk load latency.  Measured: C4 final acceptance
+// 345 -> 175 us, C4 8-GPU shard 44 -> 28 us, C5 27 -> 24 us; at C2 64 threads
+// would cost 12 -> 16 us (final) and 26 -> 47 us (exit).
+constexpr int ACC_THREADS_WIDE = 256, ACC_THREADS_NARROW = 64;
 constexpr int ACC_CHUNK = 1024;   // 32 CTAs per request at V = 32000: the race is ALU-latency bound
 
 // vocabulary chunks of ACC_CHUNK (a multiple of it for V > 32 * ACC_CHUNK): at most
@@ -20,6 +26,7 @@ struct CtaSync {
     __device__ void operator()() const { __syncthreads(); }
 };
 
+template <int ACC_THREADS>
 __global__ void __launch_bounds__(ACC_THREADS) row_stats_kernel(const __grid_constant__ AcceptArgs a) {
     __shared__ AcceptSmem S;
     pdl_launch_dependents();
@@ -33,6 +40,7 @@ __global__ void __launch_bounds__(ACC_THREADS) row_stats_kernel(const __grid_con
     gphase_mark(gtr, a.ktrace_id + 1, 5);
 }
 
+template <int ACC_THREADS>
 __global__ void __launch_bounds__(ACC_THREADS) accept_kernel(const __grid_constant__ AcceptArgs a) {
     __shared__ AcceptSmem S;
     pdl_launch_dependents();
@@ -53,19 +61,30 @@ __global__ void __launch_bounds__(ACC_THREADS) accept_kernel(const __grid_consta
 }
 
 cudaError_t accept_launch(const AcceptArgs& a, cudaStream_t st) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms < 1) sms = 148;
+    }
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(ACC_THREADS, 1, 1);
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = g_use_pdl ? 1 : 0;
     cfg.gridDim = dim3(a.B * a.G, a.nch, 1);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, row_stats_kernel, a);
+    const bool narrow_rs = a.B * a.G * a.nch > 2 * sms, narrow_acc = a.B * a.nch > 2 * sms;
+    cfg.blockDim = dim3(narrow_rs ? ACC_THREADS_NARROW : ACC_THREADS_WIDE, 1, 1);
+    cudaError_t e = narrow_rs ? cudaLaunchKernelEx(&cfg, row_stats_kernel<ACC_THREADS_NARROW>, a)
+                              : cudaLaunchKernelEx(&cfg, row_stats_kernel<ACC_THREADS_WIDE>, a);
     if (e != cudaSuccess) return e;
     cfg.gridDim = dim3(a.B, a.nch, 1);
-    return cudaLaunchKernelEx(&cfg, accept_kernel, a);
+    cfg.blockDim = dim3(narrow_acc ? ACC_THREADS_NARROW : ACC_THREADS_WIDE, 1, 1);
+    return narrow_acc ? cudaLaunchKernelEx(&cfg, accept_kernel<ACC_THREADS_NARROW>, a)
+                      : cudaLaunchKernelEx(&cfg, accept_kernel<ACC_THREADS_WIDE>, a);
 }
 
 }  // namespace sv

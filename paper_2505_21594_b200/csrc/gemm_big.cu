@@ -29,9 +29,22 @@ constexpr int GB_GROUPS = SV_GB_GROUPS;
 // SV_GTRACE buffer (tools/trace_step.py); off in the product build
 #ifdef SV_GB_TRACE
 #define GB_MARK(ph) gphase_mark(a.gtrace, a.ktrace_id, ph)
+// wait-time accounting (ns, summed over the launch's CTAs into slot (id, ph).first,
+// which starts at ~0: the stored value is sum - 1)
+#define GB_T0() const unsigned long long _gbt0 = gb_now()
+#define GB_ACC(var) var += gb_now() - _gbt0
+#define GB_FLUSH(ph, var) do { if (a.gtrace) atomicAdd(&a.gtrace[(a.ktrace_id * 16 + (ph)) * 2], var); } while (0)
 #else
 #define GB_MARK(ph) ((void)0)
+#define GB_T0() ((void)0)
+#define GB_ACC(var) ((void)0)
+#define GB_FLUSH(ph, var) ((void)0)
 #endif
+__device__ __forceinline__ unsigned long long gb_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 constexpr int GB_BK = 64;
 constexpr int GB_TM = 128;
 constexpr int GB_A = GB_TM * GB_BK * 2;
@@ -165,6 +178,8 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
             const uint32_t stage_tx = GB_A + (a.b_box ? a.b_box : TN) * GB_BK * 2;   // GemmArgs::b_box
             // weights never depend on the previous kernel: the first ring's worth of weight
             // blocks is requested before griddepcontrol.wait (streams during its tail)
+            unsigned long long w_empty = 0;
+            (void)w_empty;
             int pre = 0;
             {
                 SkPiece pc;
@@ -187,13 +202,19 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                 for (int kb = pc.kb0; kb < pc.kb1; ++kb, ++it) {
                     const int s = it % C::STAGES;
                     if (it >= pre) {
-                        if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+                        if (it >= C::STAGES) {
+                            GB_T0();
+                            mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+                            GB_ACC(w_empty);
+                        }
                         mbar_arrive_expect_tx(&full[s], stage_tx);
                         tma_load_2d(&tmA, sA + s * GB_A, &full[s], kb * GB_BK, n0, pol_w);
                     }
                     tma_load_2d(&tmB, sB + s * C::B_STAGE, &full[s], kb * GB_BK, m0 + a.b_row0, pol_x);
                 }
             }
+            GB_FLUSH(6, w_empty);
+            GB_FLUSH(10, 1ull);
             if constexpr (EPI == EPI_QKV) {   // GemmArgs::kv_pf_blocks
                 const size_t plane = (size_t)a.n_heads * EPI_PAGE * a.head_dim;   // elements per K (or V) plane
                 int item = 0;
@@ -214,16 +235,26 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
         if (lane == 0) {   // ------------------------------------------ MMA issuer
             constexpr uint32_t idesc = umma_idesc_bf16(GB_TM, TN);
             int it = 0, seg = 0;
+            unsigned long long w_full = 0, w_tempty = 0;
+            (void)w_full; (void)w_tempty;
             SkPiece pc;
             long long u;
             for (bool ok = first_piece(pc, u); ok; ok = next_piece(pc, u), ++seg) {
                 const int buf = seg & 1;
-                if (seg >= 2) mbar_wait(&tempty[buf], ((seg >> 1) - 1) & 1);
+                if (seg >= 2) {
+                    GB_T0();
+                    mbar_wait(&tempty[buf], ((seg >> 1) - 1) & 1);
+                    GB_ACC(w_tempty);
+                }
                 tc_fence_after();
                 const uint32_t dt = tmem + buf * TN;
                 for (int kb = pc.kb0; kb < pc.kb1; ++kb, ++it) {
                     const int s = it % C::STAGES;
-                    mbar_wait(&full[s], (it / C::STAGES) & 1);
+                    {
+                        GB_T0();
+                        mbar_wait(&full[s], (it / C::STAGES) & 1);
+                        if (it > 0) GB_ACC(w_full);
+                    }
                     if (it == 0) GB_MARK(2);
                     tc_fence_after();
                     const uint64_t ad = umma_sdesc_sw128(smem_u32(sA + s * GB_A));
@@ -236,6 +267,8 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
                 umma_commit(&tfull[buf]);
             }
             GB_MARK(3);
+            GB_FLUSH(7, w_full);
+            GB_FLUSH(8, w_tempty);
         }
     } else {               // ------------------------------------------ epilogue warps
         const int grp = warp >> 2, tid = threadIdx.x;     // tid 0 .. 32 * GB_EPI_WARPS - 1
@@ -246,6 +279,8 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
         pdl_wait();                                        // epilogue inputs come from earlier kernels
         const uint32_t tag = SK ? ((*a.meta.epoch << 10) | (uint32_t)(a.ktrace_id & 1023)) : 0u;
         int seg = 0;
+        unsigned long long w_tfull = 0;
+        (void)w_tfull;
         SkPiece pc;
         long long u;
         for (bool ok = first_piece(pc, u); ok; ok = next_piece(pc, u), ++seg) {
@@ -260,7 +295,11 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
             }
             epi_all_bar();
             if (tid == 0) GB_MARK(11);
-            mbar_wait(&tfull[buf], (seg >> 1) & 1);
+            {
+                GB_T0();
+                mbar_wait(&tfull[buf], (seg >> 1) & 1);
+                if (tid == 0 && seg > 0) GB_ACC(w_tfull);
+            }
             if (tid == 0) GB_MARK(13);
             tc_fence_after();
             const uint32_t tb = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + buf * TN;
@@ -329,6 +368,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
             if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
             if (tid == 0) GB_MARK(14);
         }
+        if (tid == 0) GB_FLUSH(9, w_tfull);
     }
     tc_fence_before();
     __syncthreads();
