@@ -22,6 +22,10 @@ sum_v min(p_j, q_j) = alpha.
 --impl reference runs the oracle (numpy fp64, tests-only infrastructure) on the
 host cores on a bounded sample of the same workload.
 
+The default run (C2, one GPU) also embeds `also_measured`: C5 and the per-GPU shard
+of C4 on 8 GPUs, each measured by a child bench process on the same GPU after the
+C2 timing (same timing rules; `--no-extra` skips them).
+
 Launch: python bench.py [--gpus N --steps K --warmup W] (N>1 under torchrun;
 each rank runs its own requests, no collective on the hot path; NCCL gathers
 counters once at the end).
@@ -66,6 +70,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=None, help="requests per GPU (default: per config)")
     ap.add_argument("--ctx", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="default C2 run only: skip the C5 / C4-per-GPU-shard lines embedded as `also_measured`")
     ap.add_argument("--profile-json", default=None, help="write per-launch profile records here")
     ap.add_argument("--shard", default=None, metavar="R/N",
                     help="serve rank R's requests of an N-rank job in this single process (equality tests)")
@@ -639,6 +645,12 @@ def run_ours(args):
                                              f"(alpha {args.alpha}, gamma {gamma})",
                "host": host_identity()}
 
+    also = None
+    if (world == 1 and not args.shard and not args.no_extra and args.config == "C2" and gamma == 4
+            and exit_layer == 16 and not exit_layers and not args.prefill and not args.adapters
+            and args.batch is None and args.ctx is None):
+        also = also_measured()
+
     h2d = per * gamma * mc.vocab * 4 + per * (gamma + 1) * 12   # gamma 0: no draft probabilities
     d2h = 2 * per * 64
     tau_exp = expected_tau(gamma, args.alpha)
@@ -675,9 +687,37 @@ def run_ours(args):
                          "note": "sv_prefill, one synchronous call per request, host wall clock"}
                         if prefill_s else None),
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary()}
+    if also is not None:
+        line["also_measured"] = also
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def also_measured():
+    """The default run (C2) also measures, each in a child process of this bench on the
+    same GPU after the C2 timing: C5 (SURVEY.md configs[4]) and the per-GPU shard of C4
+    on 8 GPUs (32 requests, the strong-scaling case).  A summary of each child's own
+    line (same timing rules: device events, warm-up, clocks) is embedded, so these
+    numbers carry the driver's clock too."""
+    out = {}
+    for name, argv in (("C5", ["--config", "C5", "--steps", "20", "--warmup", "3"]),
+                       ("C4_per_gpu_shard_of_8", ["--config", "C4", "--batch", "32", "--steps", "10", "--warmup", "3"])):
+        try:
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), *argv, "--no-cpu-baseline", "--no-extra"],
+                               capture_output=True, text=True, timeout=420)
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+            rf = d.get("roofline") or {}
+            out[name] = {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
+                         "latency_p50_ms": d["latency_p50_ms"], "ms_per_step": d["ms_per_step"],
+                         "steps": d["steps"], "warmup": d["warmup"],
+                         "tokens_per_step": d["tokens_per_step"], "e2e": d["e2e"],
+                         "step_frac_of_peak": rf.get("step_frac_of_peak"),
+                         "roofline": {k: rf.get(k) for k in ("bound", "achieved", "peak", "unit", "frac")},
+                         "exit_ready": d.get("exit_ready"), "clocks": d.get("clocks")}
+        except Exception as ex:   # recorded, never fatal for the C2 line
+            out[name] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+    return out
 
 
 def main():
