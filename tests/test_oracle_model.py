@@ -66,8 +66,11 @@ def _rel(a, b):
 
 
 @pytest.mark.parametrize("cfg", [tiny(),
-                                 ModelCfg(n_layers=3, d_model=256, n_heads=2, d_ff=512, vocab=384, max_ctx=128)],
-                         ids=["C1", "Dh128"])
+                                 ModelCfg(n_layers=3, d_model=256, n_heads=2, d_ff=512, vocab=384, max_ctx=128),
+                                 # the Llama2-7B layer widths (d 4096, 32 heads, F 11008, V 32000) of
+                                 # configs[1..4], 2 layers: pins the oracle's values at the bench shape
+                                 ModelCfg(n_layers=2, d_model=4096, n_heads=32, d_ff=11008, vocab=32000, max_ctx=128)],
+                         ids=["C1", "Dh128", "7B_width"])
 def test_forward_matches_hf_float64(cfg):
     m = om.Model(cfg, seed=1)
     rng = np.random.default_rng(5)
