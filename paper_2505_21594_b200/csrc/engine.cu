@@ -684,7 +684,11 @@ static int gemm_config(sv_engine* e, int M, int N, int K, bool exit_ws, GemmArgs
     // 65-80 rows (C5): 80-token tiles (UMMA N = 80) — the smaller activation stage
     // leaves room for 7 weight stages in flight instead of 6
     if (M > 64 && M <= 80 && a.M == M && !e->no_t80) tl = 80;
-    if (M > 128 && a.M == M && !e->no_wave && N < 16384) {
+    // gate/up (N = 2F) and the LM heads (N = V) too up to 320 rows: measured (same box)
+    // C4 8-GPU shard 8.19 -> 8.04 ms, 4-GPU shard 13.9 -> 13.45 ms (gate/up at 160 rows
+    // 49 -> 45 us: 160-token instead of padded 256-token tiles); at 640 rows the
+    // weighted choice (160) loses to 256 (22.1 vs 22.6 ms) and the old rule stays
+    if (M > 128 && a.M == M && !e->no_wave && (N < 16384 || M <= 320)) {
         // rounds x tile rows, weighted by the tile's MMA efficiency once the GEMM is
         // compute-bound (M >= 640): the tensor pipe is 87% busy at 256-token tiles
         // but ~50% at 128 (C4 QKV, ncu; profiles/r02/c4_tensor_pipe.json)
