@@ -7,5 +7,5 @@ run() { name=$1; shift; env "$@" timeout 300 python bench.py --no-cpu-baseline -
   python -c "
 import json; d=json.load(open('$OUT/$name.json')); k=d['roofline']['kernels']; print('%-12s p50 %.4f ms  qkv %.1f attn %.1f O %.1f gu %.1f dn %.1f us' % ('$name', d['latency_p50_ms'], *[k[x]['ms']*1e3/32 for x in ('gemm_qkv','attention','gemm_o','gemm_gate_up','gemm_down')]))" || tail -2 $OUT/$name.err; }
 for rep in 1 2 3; do
-for v in $VARS; do run ${v%%:*}$rep ${v#*:}; done
+for v in $VARS; do run ${v%%:*}$rep $(echo ${v#*:} | tr "," " "); done
 done
