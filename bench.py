@@ -66,7 +66,9 @@ def parse():
                     help="NEXT-3: exit adapters of this rank (e.g. 384) on every early exit")
     ap.add_argument("--all-exits", action="store_true",
                     help="NEXT-1: an early exit after every layer 1..L-1, streamed (overrides --exit-layer)")
-    ap.add_argument("--alpha", type=float, default=0.825)
+    ap.add_argument("--alpha", type=float, default=None,
+                    help="per-position acceptance rate of the calibrated drafts (default: 0.73 for C5 — the "
+                         "robot's tau = 2.92, PAPER.md:647 — else 0.825, tau = 3.53)")
     ap.add_argument("--batch", type=int, default=None, help="requests per GPU (default: per config)")
     ap.add_argument("--ctx", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -77,7 +79,10 @@ def parse():
                     help="serve rank R's requests of an N-rank job in this single process (equality tests)")
     ap.add_argument("--dump-results", default=None, metavar="PATH",
                     help="write every timed step's final results per request id ({rank} is substituted)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.alpha is None:   # C5 takes alpha from the robot's tau = 2.92
+        args.alpha = 0.73 if args.config == "C5" else 0.825
+    return args
 
 
 def workload(args, world):
