@@ -345,10 +345,13 @@ def run_reference(args):
     _keep = _all_host_threads()
     per, total, ctx, scaling = workload(args, 1)
     sample = OracleSample(args, ctx)
+    # bounded: at most 30 timed oracle request-steps (~1.2 s each on 16 host threads) and
+    # one warm-up, so the arm ends within a minute or two whatever --steps / --warmup are
+    n_warm, n_timed = min(args.warmup, 1), max(1, min(args.steps, 30))
     times = []
-    for i in range(args.warmup + args.steps):
+    for i in range(n_warm + n_timed):
         dt, _ = sample.step()
-        if i >= args.warmup:
+        if i >= n_warm:
             times.append(dt)
     sec = float(np.mean(times))
     tok = expected_tau(args.gamma, args.alpha)
@@ -360,7 +363,9 @@ def run_reference(args):
             "config": {"workload": f"{args.config} Llama2-7B shape, B={per}, ctx {ctx}, gamma {args.gamma}",
                        "global_batch": per, "seq_len": ctx, "parallelism": "host cores"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": desc + f"; ms_per_step = {per} request(s) x {sec * 1e3:.0f} ms; tokens/step "
+                             "sample": desc + f" (a bounded sample of the --steps {args.steps} run: "
+                                       f"{n_warm} warm-up + {n_timed} timed)"
+                                       f"; ms_per_step = {per} request(s) x {sec * 1e3:.0f} ms; tokens/step "
                                        f"{tok:.3f} = expected tau of the calibrated workload (alpha {args.alpha}, "
                                        f"gamma {args.gamma})", "host": host_identity()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
